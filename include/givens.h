@@ -1,0 +1,128 @@
+/*
+ * givens.h -- C ABI of the B200 (sm_100a) Givens library: the data-parallel hot path of
+ * arXiv 2106.00003 (Hamze, "Parallelized Computation and Backpropagation Under
+ * Angle-Parametrized Orthogonal Matrices").
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * n        matrix dimension, n >= 2. n_eff = n rounded up to even; odd n uses the bye
+ *          (phantom) index n ("bypass ... if j = n").
+ * N        number of angles = n(n-1)/2.
+ * E, theta the round-robin sequence built by the circle method (Fig. 1
+ *          PAPER.md:378-455): R = n_eff-1 blocks b_1..b_R of S = n_eff/2 disjoint pairs;
+ *          block b_{r+1} (r = 0..R-1) pairs positions k and n_eff-1-k (slot k = 0..S-1) of the
+ *          sequence s_r with s_r[0] = 0, s_r[p] = 1 + ((p-1-r) mod (n_eff-1)); each pair is
+ *          (i,j) = (min, max). theta / dtheta have length N in BLOCK-MAJOR FLAT ORDER: block
+ *          b_1 first, slots in increasing k, bye pairs skipped (reading R3).
+ *          U = prod_{e in E} G^e(theta_e) with G^{e_N} applied first, G^e as
+ *          in PAPER.md:171-181 (G_ii = G_jj = cos, G_ij = -sin, G_ji = +sin, i < j).
+ * mask     optional uint8[N] (device pointer or NULL): 1 = free angle, 0 = pinned to zero.
+ *          Pinned angles are bypassed (PAPER.md:869-872 generalised to any angle subset): their
+ *          theta value is never read (NaN is fine) and their dtheta is written as exactly 0.
+ * layout   every matrix is fp32 row-major with a leading dimension (elements) >= its row
+ *          length; X, Y, dY, dX are n x m, U is n x n. All data pointers are DEVICE pointers
+ *          (cudaMalloc / torch CUDA tensors), caller-owned; nothing is retained after return.
+ * ws       device workspace of at least givens_workspace_bytes(op, n, m) bytes, 256-byte
+ *          aligned, caller-owned; it may be reused across calls on the same stream. For
+ *          givens_backward, ws must be the SAME workspace a preceding givens_apply /
+ *          givens_build_U call with the same (n, theta, mask) filled, unless
+ *          GIVENS_FLAG_RECOMPUTE is passed (then the coefficient tables are rebuilt).
+ * stream   cudaStream_t (as void*), NULL = legacy default stream. Every call is
+ *          stream-ordered and asynchronous: it enqueues kernels and returns; results are
+ *          visible after the stream is synchronised. No call allocates device memory.
+ * errors   0 on success; negative givens_status_t otherwise, with a thread-local message
+ *          from givens_last_error(). Parameter errors are detected before anything is
+ *          enqueued. Asynchronous CUDA faults surface at the next synchronising call.
+ * threads  all functions are thread-safe (no global mutable state besides the thread-local
+ *          error string and a per-device attribute cache).
+ */
+#ifndef GIVENS_H_
+#define GIVENS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GIVENS_OK = 0,
+    GIVENS_EINVAL = -1,       /* bad argument (size, pointer, leading dimension, workspace) */
+    GIVENS_ECUDA = -2,        /* a CUDA launch / attribute call failed */
+    GIVENS_EUNSUPPORTED = -3  /* valid arguments but no kernel configuration for this n yet */
+} givens_status_t;
+
+enum { GIVENS_OP_APPLY = 0, GIVENS_OP_BUILD_U = 1, GIVENS_OP_BACKWARD = 2 };
+enum { GIVENS_FLAG_RECOMPUTE = 1 };
+
+/* Thread-local description of the last failure ("" if none). */
+const char *givens_last_error(void);
+
+/* Library version string. */
+const char *givens_version(void);
+
+/* n(n-1)/2, or -1 if n < 2. */
+int64_t givens_num_angles(int32_t n);
+
+/* 1 if the GPU path supports dimension n (a kernel configuration exists), else 0. */
+int givens_supported(int32_t n);
+
+/*
+ * Host-side, pure: the circle-method schedule by its closed form (Fig. 1).
+ * pairs_host: int32[R][S][2] (i < j; bye pairs of odd n have j == n), flat_host: int64[R][S]
+ * (flat angle index, -1 for the bye). Either may be NULL. Returns 0 or GIVENS_EINVAL.
+ */
+int givens_schedule(int32_t n, int32_t *pairs_host, int64_t *flat_host);
+
+/*
+ * Host-side, pure: mask[N] from an excluded-dimension set excluded_dims_host[n] (1 =
+ * excluded): pair (i,j) is pinned iff both i and j are excluded. The paper's §5 restriction
+ * is excluded = {m_keep, ..., n-1}.
+ */
+int givens_mask_from_dims(int32_t n, const uint8_t *excluded_dims_host, uint8_t *mask_host);
+
+/* Workspace bytes for op (GIVENS_OP_*) at (n, m). Returns 0 for invalid arguments. */
+size_t givens_workspace_bytes(int op, int32_t n, int64_t m);
+
+/*
+ * Y = U(theta) X (transpose = 0) or Y = U(theta)^T X (transpose = 1): Algorithm 2
+ * applied to the columns of X instead of I. Y may alias X (same pointer
+ * and leading dimension). Fills the coefficient tables in ws (reused by givens_backward).
+ */
+int givens_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask,
+                 const float *X, int64_t ldx, float *Y, int64_t ldy, int transpose,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* U = U(theta), n x n (Algorithm 2 from U <- I_n). Fills ws tables. */
+int givens_build_U(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu,
+                   void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Backward of Y = U(theta) X given Y and dY = dL/dY (n x m):
+ *   dtheta[N] = dL/dtheta (overwritten, never accumulated; masked entries exactly 0),
+ *   dX = U^T dY (optional, NULL to skip; may alias dY).
+ * Activations are replayed from Y by inverse rotation (U^fwd recursion),
+ * each dtheta_e is reduced over the m columns with a fixed-order, atomic-free two-stage sum
+ * (PAPER.md:768-781), so the result is bitwise deterministic for a given (n, m, device).
+ * With X = I, Y = U, dY = Gamma this is the paper's Algorithm 3.
+ * flags: GIVENS_FLAG_RECOMPUTE rebuilds the coefficient tables from theta/mask.
+ */
+int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mask,
+                    const float *Y, int64_t ldy, const float *dY, int64_t lddy,
+                    float *dX, int64_t lddx, float *dtheta, int flags,
+                    void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Debug / test: run the kernels' data movement for dimension n with row ids as data and no
+ * rotation, and record, for every block b_{r+1} and slot k, the row ids the kernel pairs:
+ * out_dev int32[R][S][2] (device), reported as (min, max). direction 0 walks the blocks in
+ * forward order (b_R first, as givens_apply), 1 in backward order (b_1 first, as
+ * givens_backward). Bit-exact against the schedule (pins the on-device indexing).
+ */
+int givens_index_trace(int32_t n, int direction, int32_t *out_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GIVENS_H_ */

@@ -1,0 +1,178 @@
+"""PyTorch-facing ops over the C ABI (include/givens.h).
+
+PyTorch supplies device memory, streams and process groups; every step of the method runs in
+libgivens.so's sm_100a kernels. These wrappers only check shapes/dtypes and marshal pointers.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import FLAG_RECOMPUTE, OP_APPLY, OP_BACKWARD, OP_BUILD_U, check, lib
+
+
+def num_angles(n: int) -> int:
+    """N = n(n-1)/2."""
+    v = int(lib().givens_num_angles(n))
+    if v < 0:
+        raise ValueError(f"n must be >= 2 (got {n})")
+    return v
+
+
+def n_eff(n: int) -> int:
+    return n + (n % 2)
+
+
+def schedule(n: int):
+    """Circle-method schedule (closed form, host side): pairs int32[R][S][2], flat int64[R][S]."""
+    ne = n_eff(n)
+    R, S = ne - 1, ne // 2
+    pairs = np.zeros((R, S, 2), dtype=np.int32)
+    flat = np.zeros((R, S), dtype=np.int64)
+    check(lib().givens_schedule(n, pairs.ctypes.data_as(ctypes.c_void_p), flat.ctypes.data_as(ctypes.c_void_p)))
+    return pairs, flat
+
+
+def mask_from_dims(n: int, excluded) -> np.ndarray:
+    """uint8 mask[N]: pair (i,j) pinned iff both i and j are in the excluded dimension set."""
+    ex = np.zeros(n, dtype=np.uint8)
+    ex[np.asarray(list(excluded), dtype=np.int64)] = 1
+    mask = np.zeros(num_angles(n), dtype=np.uint8)
+    check(lib().givens_mask_from_dims(n, ex.ctypes.data_as(ctypes.c_void_p), mask.ctypes.data_as(ctypes.c_void_p)))
+    return mask
+
+
+def mask_from_keep(n: int, m_keep: int) -> np.ndarray:
+    """Paper §5: exclude every pair inside {m_keep, ..., n-1}."""
+    return mask_from_dims(n, range(m_keep, n))
+
+
+def workspace_bytes(op: int, n: int, m: int) -> int:
+    return int(lib().givens_workspace_bytes(op, n, m))
+
+
+def workspace(op: int, n: int, m: int, device=None) -> torch.Tensor:
+    nb = workspace_bytes(op, n, m)
+    if nb == 0:
+        raise ValueError(f"bad workspace query op={op} n={n} m={m}")
+    return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(dev) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _check_matrix(name, t, n):
+    if not (t.is_cuda and t.dtype == torch.float32 and t.dim() == 2 and t.shape[0] == n and t.stride(1) == 1):
+        raise ValueError(f"{name} must be a CUDA float32 [n, m] tensor with unit column stride "
+                         f"(got {tuple(t.shape)} {t.dtype} {t.device} strides {t.stride()})")
+
+
+def _check_theta(theta, mask, n):
+    N = num_angles(n)
+    if not (theta.is_cuda and theta.dtype == torch.float32 and theta.is_contiguous() and theta.numel() == N):
+        raise ValueError(f"theta must be a contiguous CUDA float32 tensor of {N} angles")
+    if mask is not None and not (mask.is_cuda and mask.dtype == torch.uint8 and mask.is_contiguous()
+                                 and mask.numel() == N):
+        raise ValueError(f"mask must be a contiguous CUDA uint8 tensor of {N} entries")
+
+
+def apply(theta: torch.Tensor, X: torch.Tensor, mask: torch.Tensor | None = None, transpose: bool = False,
+          out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """Y = U(theta) X (or U^T X): Algorithm 2 on the columns of X."""
+    n, m = X.shape
+    _check_matrix("X", X, n)
+    _check_theta(theta, mask, n)
+    Y = torch.empty_like(X) if out is None else out
+    _check_matrix("out", Y, n)
+    if ws is None:
+        ws = workspace(OP_APPLY, n, m, X.device)
+    check(lib().givens_apply(n, m, _ptr(theta), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y), Y.stride(0),
+                             int(bool(transpose)), _ptr(ws), ws.numel(), _stream(X.device)))
+    return Y
+
+
+def build_U(theta: torch.Tensor, n: int, mask: torch.Tensor | None = None, out: torch.Tensor | None = None,
+            ws: torch.Tensor | None = None) -> torch.Tensor:
+    """U = U(theta) (Algorithm 2 from U <- I_n)."""
+    _check_theta(theta, mask, n)
+    U = torch.empty((n, n), dtype=torch.float32, device=theta.device) if out is None else out
+    _check_matrix("U", U, n)
+    if ws is None:
+        ws = workspace(OP_BUILD_U, n, n, theta.device)
+    check(lib().givens_build_U(n, _ptr(theta), _ptr(mask), _ptr(U), U.stride(0), _ptr(ws), ws.numel(),
+                               _stream(theta.device)))
+    return U
+
+
+def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch.Tensor | None = None,
+             want_dX: bool = True, ws: torch.Tensor | None = None, recompute: bool = True,
+             dtheta: torch.Tensor | None = None, dX: torch.Tensor | None = None):
+    """(dtheta, dX) for Y = U(theta) X given Y and dY (replay backward, §4).
+
+    recompute=False reuses the coefficient tables a preceding apply/build_U left in `ws`
+    (ws must then be a backward-sized workspace that the forward used)."""
+    n, m = Y.shape
+    _check_matrix("Y", Y, n)
+    _check_matrix("dY", dY, n)
+    _check_theta(theta, mask, n)
+    if ws is None:
+        ws = workspace(OP_BACKWARD, n, m, Y.device)
+        recompute = True
+    if dtheta is None:
+        dtheta = torch.empty(num_angles(n), dtype=torch.float32, device=Y.device)
+    if want_dX and dX is None:
+        dX = torch.empty_like(dY)
+    if dX is not None:
+        _check_matrix("dX", dX, n)
+    check(lib().givens_backward(n, m, _ptr(theta), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY), dY.stride(0),
+                                _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
+                                FLAG_RECOMPUTE if recompute else 0, _ptr(ws), ws.numel(), _stream(Y.device)))
+    return dtheta, dX
+
+
+def index_trace(n: int, direction: int = 0, device=None) -> torch.Tensor:
+    """Row ids the kernels pair per (block, slot), as (min, max): int32 [R][S][2] (device)."""
+    ne = n_eff(n)
+    out = torch.full((ne - 1, ne // 2, 2), -1, dtype=torch.int32, device=device or "cuda")
+    check(lib().givens_index_trace(n, int(direction), _ptr(out), _stream(out.device)))
+    return out
+
+
+class GivensApply(torch.autograd.Function):
+    """Y = U(theta) X with the replay backward. The forward's coefficient tables are kept in a
+    backward-sized workspace and reused by the backward (no recompute)."""
+
+    @staticmethod
+    def forward(ctx, theta, X, mask=None):
+        n, m = X.shape
+        ws = workspace(OP_BACKWARD, n, m, X.device)
+        Y = apply(theta, X, mask=mask, ws=ws)
+        ctx.save_for_backward(theta, Y, mask if mask is not None else torch.empty(0, device=X.device))
+        ctx.ws = ws
+        ctx.has_mask = mask is not None
+        return Y
+
+    @staticmethod
+    def backward(ctx, dY):
+        theta, Y, mask = ctx.saved_tensors
+        mask = mask if ctx.has_mask else None
+        dY = dY.contiguous()
+        dtheta, dX = backward(theta, Y, dY, mask=mask, want_dX=ctx.needs_input_grad[1], ws=ctx.ws, recompute=False)
+        return dtheta, dX, None
+
+
+def givens_apply(theta, X, mask=None):
+    """Differentiable Y = U(theta) X."""
+    return GivensApply.apply(theta, X, mask)
+
+
+def version() -> str:
+    return lib().givens_version().decode()
