@@ -1,0 +1,332 @@
+#!/usr/bin/env python
+"""Benchmark of the data-parallel hot path of arXiv 2106.00003 on B200.
+
+One step = the whole hot path on one batch: coefficient precompute (schedule + cos/sin
+table), forward Y = U(theta) X (all n-1 blocks), replay backward (dX, dtheta with the
+two-stage reduction) and, for N > 1, the NCCL all_reduce of dtheta. Workload (BASELINE.json
+configs[2], "C3"): n = 1024, m = 65536 columns, fp32, synthetic seeded inputs; m is sharded
+over the N ranks (strong scaling: the total m is fixed).
+
+metric = Givens rotations/s fwd+bwd: units = N_angles * m (one 2x2 rotation applied to one
+column, forward and backward); value = units / (max-over-ranks device time
+per step).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+--impl reference times the fp64 CPU oracle (the only reference this paper has: it released no
+code) on the host cores, on a bounded column sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Givens rotations/s fwd+bwd at n=1024 (1/2/4/8 B200); U-build ms vs n"
+UNIT = "rotations/s"
+N_DIM = 1024
+M_TOTAL = 65536
+SEED = 0
+FP32_LANES_PER_SM = 128           # B200 SM: 4 SMSP x 32 FP32 lanes (B200_PROFILING.md / guide)
+FLOPS_FWD, FLOPS_BWD = 6, 16      # algorithmic flops per rotation-column
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_DIM)
+    ap.add_argument("--m", type=int, default=M_TOTAL)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample-cols", type=int, default=1024)
+    ap.add_argument("--ref-cols-per-step", type=int, default=128)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts[5:9]))
+            except ValueError:
+                continue
+        if not rows:
+            return None
+        mx = max(r[1] for r in rows)
+        load = [r[0] for r in rows if r[0] > 0.5 * mx] or [r[0] for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ reference arm (CPU oracle)
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    import synth
+    n, m = args.n, args.m
+    N = n * (n - 1) // 2
+    cols = args.ref_cols_per_step
+    th = synth.theta(N, seed=SEED)
+    times = []
+    for s in range(args.warmup + args.steps):
+        c0 = (s * cols) % m
+        X = synth.normal_matrix(n, m, SEED, synth.TID_X, c0, c0 + cols).astype(np.float64)
+        dY = synth.normal_matrix(n, m, SEED, synth.TID_DY, c0, c0 + cols).astype(np.float64)
+        t0 = time.perf_counter()
+        oracle.apply(n, th, X)
+        oracle.backward(n, th, X, dY)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    value = N * cols / t
+    cores = oracle.num_threads()
+    sample = f"{cols} of {m} columns per step (n={n}), fp64 oracle: Alg. 1 forward + taped reverse-mode backward"
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C3: n={n}, m={m} fwd+bwd (column sample per step)", "n": n, "m": m,
+                   "sample_cols_per_step": cols},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(args):
+    import numpy as np
+
+    import oracle
+    import synth
+    n = args.n
+    N = n * (n - 1) // 2
+    cols = args.cpu_sample_cols
+    th = synth.theta(N, seed=SEED)
+    X = synth.normal_matrix(n, args.m, SEED, synth.TID_X, 0, cols).astype(np.float64)
+    dY = synth.normal_matrix(n, args.m, SEED, synth.TID_DY, 0, cols).astype(np.float64)
+    t0 = time.perf_counter()
+    oracle.apply(n, th, X)
+    oracle.backward(n, th, X, dY)
+    t = time.perf_counter() - t0
+    return {"value": N * cols / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"first {cols} of {args.m} columns (n={n}): fp64 Alg. 1 forward + taped backward, "
+                      f"{t:.1f} s wall"}
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2106_00003_b200 as g
+    from paper_2106_00003_b200.dist import allreduce_dtheta, shard_columns
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n, m_total = args.n, args.m
+    N = n * (n - 1) // 2
+    c0, c1 = shard_columns(m_total, rank, world)
+    m = c1 - c0
+
+    # seeded synthetic inputs, generated for this rank's column shard only
+    th_h = synth.theta(N, seed=SEED)
+    X_h = synth.normal_matrix(n, m_total, SEED, synth.TID_X, c0, c1)
+    dY_h = synth.normal_matrix(n, m_total, SEED, synth.TID_DY, c0, c1)
+    theta = torch.from_numpy(th_h).to(dev)
+    X = torch.from_numpy(X_h).to(dev)
+    dY = torch.from_numpy(dY_h).to(dev)
+    Y = torch.empty_like(X)
+    dX = torch.empty_like(X)
+    dtheta = torch.empty(N, dtype=torch.float32, device=dev)
+    ws = g.workspace(g.OP_BACKWARD, n, m, dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        g.apply(theta, X, out=Y, ws=ws)                                  # precompute + forward
+        e_b0.record(stream)
+        g.backward(theta, Y, dY, ws=ws, recompute=False, dtheta=dtheta, dX=dX)  # replay bwd + stage 2
+        e_b1.record(stream)
+        if world > 1:
+            allreduce_dtheta(dtheta)
+
+    e_b0 = torch.cuda.Event(enable_timing=True)
+    e_b1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    bwd_ms = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(float(k))          # L2 flush between timed steps (outside the step events)
+        starts[k].record(stream)
+        step()
+        ends[k].record(stream)
+        e_b1.synchronize()
+        bwd_ms.append(e_b0.elapsed_time(e_b1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t_rank = torch.tensor([sum(step_ms) / len(step_ms), sum(bwd_ms) / len(bwd_ms)], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_rank, op=dist.ReduceOp.MAX)
+    ms_step, ms_bwd = float(t_rank[0]), float(t_rank[1])
+    units = N * m_total
+    value = units / (ms_step * 1e-3)
+
+    # ---------------- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xp = torch.from_numpy(X_h).pin_memory()
+        dYp = torch.from_numpy(dY_h).pin_memory()
+        dth_p = torch.empty(N, dtype=torch.float32).pin_memory()
+        Xd = torch.empty_like(X)
+        dYd = torch.empty_like(dY)
+
+        def e2e_step():
+            Xd.copy_(Xp, non_blocking=True)
+            dYd.copy_(dYp, non_blocking=True)
+            Yd = g.apply(theta, Xd, ws=ws)
+            d, _ = g.backward(theta, Yd, dYd, ws=ws, recompute=False, want_dX=True)
+            if world > 1:
+                allreduce_dtheta(d)
+            dth_p.copy_(d, non_blocking=True)
+            return d
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        ks = max(3, args.steps // 2)
+        if world > 1:
+            dist.barrier()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        es.record(stream)
+        for _ in range(ks):
+            e2e_step()
+        ee.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([es.elapsed_time(ee) / ks], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": units / (float(te[0]) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 4 * n * m,
+               "d2h_bytes_per_step": 4 * N, "ms_per_step": float(te[0])}
+
+    if rank == 0:
+        sm_mhz = (clk or {}).get("sm_mhz")
+        peak_clock = 1965.0
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak = n_sm * FP32_LANES_PER_SM * 2 * peak_clock * 1e6 / 1e12   # TFLOP/s at max boost clock
+        achieved = FLOPS_BWD * N * m / (ms_bwd * 1e-3) / 1e12
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "bwd_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"C3: n={n}, m={m_total} fwd+bwd (precompute + forward + replay backward"
+                                   f"{' + NCCL all_reduce(dtheta)' if world > 1 else ''}), m sharded over ranks",
+                       "n": n, "m": m_total, "m_per_rank": m, "angles": N,
+                       "l2": "flushed between steps (256 MiB write outside the step events); X is 256 MiB at N=1",
+                       "seed": SEED, "parallelism": f"dp{world}"},
+            "roofline": {"bound": "alu", "kernel": "givens_backward (k_ring<16,BWD> + k_dtheta_reduce)",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic,
+                         "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {peak_clock:.0f} MHz "
+                                       "(max boost; DESIGN.md §5)",
+                         "flops_per_rotation_column": FLOPS_BWD, "ms_per_launch": ms_bwd},
+            "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd,
+            "gpu_launches": 6 * args.steps,
+            "clocks": clk,
+        }
+        if e2e:
+            out["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -5,7 +5,7 @@
 // Kernels (DESIGN.md §4 lists the roofline and algorithmic bytes of each):
 //   k_flip / k_sigma / k_coef  per-call coefficient precompute (fp64 trig, pi-reduction, sign
 //                              bookkeeping) into the ring kernels' lane-chunked table layout;
-//   k_ring<W,K,MODE>           the hot path: one CTA owns a column slab, every block b_r runs
+//   k_ring<W,L,MODE>           the hot path: one CTA owns a column slab, every block b_r runs
 //                              on-chip from registers, coefficients stream in by TMA bulk copies;
 //   k_generic<MODE>            any-n fallback (pairs derived lazily per block);
 //   k_dtheta_reduce            stage 2 of the dtheta reduction (fixed CTA order, no atomics);
@@ -18,6 +18,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
+#include <utility>
 #include <mutex>
 #include <string>
 
@@ -81,7 +83,6 @@ __host__ __device__ __forceinline__ int pos_of(int i, int r, int ne) {
 struct Cfg {
     int ne, S, R, W, L, fast;  // fast: register ring kernel (else generic)
     int rowbytes;              // bytes per table row (S float2, padded to 16)
-    int sps;                   // table rows per TMA stage
 };
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
@@ -101,20 +102,12 @@ Cfg make_cfg(int n) {
     } else if (c.S == 1024) {
         c.fast = 1; c.W = 32; c.L = 32;
     }
-    c.rowbytes = ((c.S * 8) + 15) / 16 * 16;
-    int sps = 1;
-    if (c.fast) {
-        sps = c.W / 2;
-        while (sps > 1 && (int64_t)sps * c.rowbytes > 32768) sps /= 2;
-    }
-    c.sps = sps;
+    c.rowbytes = ((c.S * 8) + 15) / 16 * 16;  // == S*8 for every ring configuration
     return c;
 }
 
 constexpr int kNW = 8;           // warps per CTA of the ring kernel
 constexpr int kThreads = kNW * 32;
-constexpr int kNStage = 3;       // coefficient stages in flight
-constexpr int kNRB = 3;          // dtheta step buffers in flight
 
 enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3 };
 
@@ -135,13 +128,6 @@ int dev_sms() {
         cache[d] = v;
     }
     return cache[d];
-}
-
-size_t ring_smem_bytes(const Cfg &c, int mode) {
-    size_t b = 256;  // barriers
-    b += (size_t)kNStage * c.sps * c.rowbytes;
-    if (mode == M_BWD) b += (size_t)kNRB * kNW * c.S * 4;
-    return b;
 }
 
 int64_t cols_per_slab(const Cfg &c, int mode) {
@@ -201,14 +187,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t *b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+__device__ __forceinline__ bool mbar_try(uint64_t *b, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
-        "r"(parity)
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+// structured (C++-level) spin so the compiler sees the loop and re-converges the warp after it
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    while (!mbar_try(b, parity)) {
+    }
+}
+
+// compile-time unrolling: f(std::integral_constant<int, I>{}) for I = 0..N-1, as straight-line code
+template <typename F, int... I>
+__device__ __forceinline__ void unroll_impl(F &&f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void unroll(F &&f) {
+    unroll_impl(f, std::make_integer_sequence<int, N>{});
 }
 __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
     asm volatile(
@@ -291,8 +294,8 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
 // ------------------------------------------------------------------ stage-2 dtheta reduction
 // dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in fixed CTA order (PAPER.md:768-781
 // "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0.
-__global__ void k_dtheta_reduce(int S, int G, const float *__restrict__ partial, const int32_t *__restrict__ amap,
-                                float *__restrict__ dtheta) {
+__global__ void k_dtheta_reduce(int S, int W, int L, int G, const float *__restrict__ partial,
+                                const int32_t *__restrict__ amap, float *__restrict__ dtheta) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int rows = 2 * S;
     if (idx >= (int64_t)rows * S) return;
@@ -303,8 +306,13 @@ __global__ void k_dtheta_reduce(int S, int G, const float *__restrict__ partial,
         dtheta[f] = 0.f;
         return;
     }
+    int rho = (int)(idx / S), k = (int)(idx % S);
+    // partial rows are stored in the ring kernel's chunk order: chunk (q/4)*L + t holds slots
+    // t*W + 4*(q/4) + 0..3 (natural order when L = 1, W = S)
+    int t = k / W, q = k % W;
+    int pos = (((q >> 2) * L + t) << 2) + (q & 3);
     float s = 0.f;
-    const float *p = partial + idx;
+    const float *p = partial + (int64_t)rho * S + pos;
     int64_t stride = (int64_t)rows * S;
     for (int c = 0; c < G; c++) s += p[(int64_t)c * stride];
     dtheta[f] = (code & (1 << 30)) ? -s : s;
@@ -312,7 +320,7 @@ __global__ void k_dtheta_reduce(int S, int G, const float *__restrict__ partial,
 
 // ------------------------------------------------------------------ the register-ring kernel
 struct RingArgs {
-    int n, ne, S, L, rowbytes, sps;
+    int n, ne;
     int64_t m;
     const float *X;   // FWD/TRANS: input; BWD: Y
     int64_t ldx;
@@ -322,7 +330,7 @@ struct RingArgs {
     int64_t ldy;
     const uint8_t *coef;
     const uint8_t *sfin;
-    float *partial;   // BWD: [grid][2S][S]
+    float *partial;   // BWD: [grid][2S][S] in chunk order (see chunk_pos)
     int64_t nslabs;
     int vec_ok;       // 1 if all row starts are 16-byte aligned for K-wide vector access
 };
@@ -392,101 +400,155 @@ struct ColIO<4> {
 template <typename V>
 __device__ __forceinline__ V vneg_if(V v, bool neg) { return neg ? neg_v(v) : v; }
 
-template <int W, int MODE>
+__device__ __forceinline__ void bulk_s2g_reduce_add(float *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_store(float *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Compile-time geometry of one ring configuration (W slots per lane, L lanes per column group).
+template <int W, int L, int MODE>
+struct RingGeom {
+    static constexpr int S = W * L;                 // slots = n_eff / 2
+    static constexpr int STEPS = 2 * S;             // pad + the R = 2S-1 blocks
+    static constexpr int LC = 32 / L;               // column groups per warp
+    static constexpr int K = kcols(W, MODE);        // columns per thread
+    static constexpr int SPS = (W >= 32) ? 4 : W / 2;   // table rows per TMA stage (divides W)
+    static constexpr int ROWB = S * 8;              // bytes per table row
+    static constexpr int STAGEB = SPS * ROWB;
+    static constexpr int NSTAGE = (S >= 1024) ? 2 : 3;
+    static constexpr int D = 4;                     // dtheta step ring depth (divides W)
+    static constexpr int LAG = 2;                   // a step is reduced LAG steps after it is written
+    static constexpr int NCH = S / 4;               // float4 chunks of a step's per-slot sums
+    static constexpr int OUTCH = (NCH + kNW - 1) / kNW;  // chunks reduced per warp (max)
+    static constexpr bool GRAD = (MODE == M_BWD);
+    static constexpr size_t OFF_STAGE = 256;
+    static constexpr size_t OFF_RED = OFF_STAGE + (size_t)NSTAGE * STAGEB;
+    static constexpr size_t OFF_OUT = OFF_RED + (GRAD ? (size_t)kNW * D * NCH * 16 : 0);
+    static constexpr size_t SMEM = OFF_OUT + (GRAD ? (size_t)kNW * D * OUTCH * 16 : 0);
+};
+
+// Hot-path kernel. One CTA of kNW warps owns a slab of C = kNW * LC * K columns; every column
+// lives in the registers of L lanes (ring.cuh). All 2S steps (pad + the n_eff-1 blocks) run
+// on-chip; the coefficient table streams through shared memory in TMA bulk stages; the
+// backward's per-slot column sums are reduced across warps LAG steps later and leave the SM
+// as TMA bulk reduce-adds into this CTA's private partial row (fixed order => deterministic).
+template <int W, int L, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
-    constexpr int K = kcols(W, MODE);
-    using IO = ColIO<K>;
+    using G = RingGeom<W, L, MODE>;
+    using IO = ColIO<G::K>;
     using V = typename IO::V;
     constexpr int KP = IO::KP;
+    constexpr int K = G::K;
+    constexpr int S = G::S, STEPS = G::STEPS, LC = G::LC, SPS = G::SPS, NSTAGE = G::NSTAGE;
+    constexpr int D = G::D, LAG = G::LAG, NCH = G::NCH, OUTCH = G::OUTCH;
     constexpr bool UP = (MODE == M_TRANS || MODE == M_BWD);  // walk b_1 -> b_R (inverse rotations)
-    constexpr bool GRAD = (MODE == M_BWD);
+    constexpr bool GRAD = G::GRAD;
+    static_assert(W % SPS == 0 && W % D == 0 && W % 4 == 0, "geometry");
 
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + kNStage;
-    uint64_t *rfull = empty + kNStage;
-    uint64_t *rempty = rfull + kNRB;
-    uint8_t *stagebuf = smem + 256;
-    float *red = reinterpret_cast<float *>(stagebuf + (size_t)kNStage * a.sps * a.rowbytes);
+    uint64_t *empty = full + NSTAGE;
+    uint64_t *rfull = empty + NSTAGE;
+    uint64_t *rempty = rfull + D;
+    uint8_t *stagebuf = smem + G::OFF_STAGE;
+    float4 *red = reinterpret_cast<float4 *>(smem + G::OFF_RED);   // [kNW][D][NCH]
+    float4 *outb = reinterpret_cast<float4 *>(smem + G::OFF_OUT);  // [kNW][D][OUTCH]
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int L = a.L, Lc = 32 / L;
     const int g = lane / L, t = lane % L;
     const bool first = (t == 0), last = (t == L - 1);
-    const int S = a.S, ne = a.ne, n = a.n;
-    const int sps = a.sps;
-    const int steps = 2 * S;             // pad + R blocks
-    const int nst = steps / sps;         // stages per slab
-    const int64_t C = (int64_t)kNW * Lc * K;
-    const int64_t my_slabs = (a.nslabs - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    const int64_t total_stages = my_slabs * nst;
-    const uint32_t stage_bytes = (uint32_t)(sps * a.rowbytes);
+    const int ne = a.ne, n = a.n;
+    const int64_t C = (int64_t)kNW * LC * K;
+    const int my_slabs = (int)((a.nslabs - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int total_stages = my_slabs * (STEPS / SPS);
+    const int total_steps = my_slabs * STEPS;
+    // chunk range of the per-step sums this warp reduces
+    const int ch0 = (warp * NCH) / kNW, ch1 = ((warp + 1) * NCH) / kNW;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kNStage; i++) {
+        for (int i = 0; i < NSTAGE; i++) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], kNW);
         }
-        for (int i = 0; i < kNRB; i++) {
+        for (int i = 0; i < D; i++) {
             mbar_init(&rfull[i], kNW);
             mbar_init(&rempty[i], kNW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        fence_proxy_async_smem();
     }
     __syncthreads();
 
-    // table rows of stage j (slab-local): forward reads rho = 2S - u (descending), backward rho = u
-    auto stage_src = [&](int64_t gstage) -> const uint8_t * {
-        int j = (int)(gstage % nst);
-        int rho0 = UP ? j * sps : (steps - (j + 1) * sps + 1);
-        return a.coef + (int64_t)rho0 * a.rowbytes;
+    // table rows of slab-local stage j: forward reads rho = 2S - u (descending), backward rho = u
+    auto stage_src = [&](int gst) -> const uint8_t * {
+        int j = gst % (STEPS / SPS);
+        int rho0 = UP ? j * SPS : (STEPS - (j + 1) * SPS + 1);
+        return a.coef + (int64_t)rho0 * G::ROWB;
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kNStage - 1 && s < total_stages; s++) {
-            mbar_expect_tx(&full[s], stage_bytes);
-            bulk_g2s(stagebuf + (size_t)s * stage_bytes, stage_src(s), stage_bytes, &full[s]);
+        for (int s = 0; s < NSTAGE - 1 && s < total_stages; s++) {
+            mbar_expect_tx(&full[s], G::STAGEB);
+            bulk_g2s(stagebuf + (size_t)s * G::STAGEB, stage_src(s), G::STAGEB, &full[s]);
         }
     }
 
-    int64_t gstage = 0;  // stages consumed by this CTA
-    int64_t gstep = 0;   // steps completed by this CTA (for dtheta step buffers)
+    // dtheta stage 1: reduce global step gs (its per-warp sums sit in ring slot gs % D) over the
+    // kNW warps for this warp's chunk range and push it to this CTA's partial row.
+    auto reduce_step = [&](int gs) {
+        const int d = gs % D;
+        mbar_wait(&rfull[d], (uint32_t)((gs / D) & 1));
+        __syncwarp();
+        const int rho = gs % STEPS;
+        const bool first_slab = gs < STEPS;
+        float4 *ob = outb + ((size_t)warp * D + d) * OUTCH;
+        if (lane == 0) bulk_wait_read<D - 1>();   // the bulk op that last read ob has finished
+        __syncwarp();
+        const int ci = ch0 + lane;
+        if (ci < ch1) {
+            float4 s = red[((size_t)0 * D + d) * NCH + ci];
+#pragma unroll
+            for (int w = 1; w < kNW; w++) {
+                float4 v = red[((size_t)w * D + d) * NCH + ci];
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+            }
+            ob[lane] = s;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&rempty[d]);
+            if (ch1 > ch0) {
+                fence_proxy_async_smem();
+                float *dst = a.partial + ((int64_t)blockIdx.x * STEPS + rho) * S + ch0 * 4;
+                if (first_slab) bulk_s2g_store(dst, ob, (uint32_t)(ch1 - ch0) * 16);
+                else bulk_s2g_reduce_add(dst, ob, (uint32_t)(ch1 - ch0) * 16);
+                bulk_commit();
+                // successive slabs add into the same partial row: keep them ordered
+                if (rho == STEPS - 1) bulk_wait_all();
+            }
+        }
+    };
+
+    int gst = 0;    // coefficient stages consumed by this CTA
+    int gstep = 0;  // steps completed by this CTA
     V ZT[KP][W], ZB[KP][W];
     V DT[GRAD ? KP : 1][GRAD ? W : 1], DB[GRAD ? KP : 1][GRAD ? W : 1];
 
-    // reduce (stage 1 across the CTA's warps) the dtheta partials of global step gs
-    auto reduce_step = [&](int64_t gs) {
-        int rb = (int)(gs % kNRB);
-        mbar_wait(&rfull[rb], (uint32_t)((gs / kNRB) & 1));
-        int64_t slab_i = gs / steps;   // local slab ordinal
-        int rho = (int)(gs % steps);
-        const float4 *src = reinterpret_cast<const float4 *>(red + (size_t)rb * kNW * S);
-        float4 *dst = reinterpret_cast<float4 *>(a.partial + ((int64_t)blockIdx.x * steps + rho) * S);
-        const int nchunks = S / 4;
-        for (int ci = threadIdx.x; ci < nchunks; ci += kThreads) {
-            float4 s = src[ci];
-#pragma unroll
-            for (int w = 1; w < kNW; w++) {
-                float4 v = src[(size_t)w * nchunks + ci];
-                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-            }
-            // chunk ci = (q/4)*L + t  ->  slots t*W + 4*(ci/L) + 0..3
-            int tt = ci % L, qq = (ci / L) * 4;
-            int k0 = tt * W + qq;
-            float4 *d = dst + k0 / 4;
-            if (slab_i > 0) {
-                float4 o = *d;
-                s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
-            }
-            *d = s;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&rempty[rb]);
-    };
-
     for (int64_t slab = blockIdx.x; slab < a.nslabs; slab += gridDim.x) {
-        const int64_t col0 = slab * C + (int64_t)(warp * Lc + g) * K;
-        // ---------------- load the slab into the start layout
+        const int64_t col0 = slab * C + (int64_t)(warp * LC + g) * K;
+        // ---------------- load the slab into the start layout (s_0 forward, s_{R-1} backward)
 #pragma unroll
         for (int q = 0; q < W; q++) {
             const int k = t * W + q;
@@ -498,19 +560,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
             if constexpr (MODE == M_BUILDU) {
 #pragma unroll
                 for (int p = 0; p < KP; p++) {
-                    float e[2];
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        int64_t c = col0 + 2 * p + h;
-                        e[h] = (rt < n && c == rt) ? 1.f : 0.f;
-                    }
-                    vt[p] = make_float2(e[0], e[1]);
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        int64_t c = col0 + 2 * p + h;
-                        e[h] = (rb < n && c == rb) ? 1.f : 0.f;
-                    }
-                    vb[p] = make_float2(e[0], e[1]);
+                    const int64_t c = col0 + 2 * p;
+                    vt[p] = make_float2((rt < n && c == rt) ? 1.f : 0.f, (rt < n && c + 1 == rt) ? 1.f : 0.f);
+                    vb[p] = make_float2((rb < n && c == rb) ? 1.f : 0.f, (rb < n && c + 1 == rb) ? 1.f : 0.f);
                 }
             } else {
                 if (rt < n) IO::load(a.X + (int64_t)rt * a.ldx, col0, a.m, a.vec_ok, vt);
@@ -519,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
             }
             if (UP) {
-                bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }
@@ -530,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                 else for (int p = 0; p < KP; p++) vt[p] = V{};
                 if (rb < n) IO::load(a.dY + (int64_t)rb * a.lddy, col0, a.m, a.vec_ok, vb);
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
-                bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
 #pragma unroll
                 for (int p = 0; p < KP; p++) {
                     DT[p][q] = vneg_if(vt[p], nt);
@@ -539,15 +591,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
             }
         }
 
-        // ---------------- all 2S steps (pad + the R blocks), W steps per unrolled body
-        for (int body = 0; body < steps / W; body++) {
-#pragma unroll
-            for (int uu = 0; uu < W; uu++) {
-                const int su = uu % sps;
-                if (su == 0) mbar_wait(&full[gstage % kNStage], (uint32_t)((gstage / kNStage) & 1));
-                const uint8_t *rowp = stagebuf + (size_t)(gstage % kNStage) * stage_bytes +
-                                      (size_t)(UP ? su : (sps - 1 - su)) * a.rowbytes;
-                const float4 *row4 = reinterpret_cast<const float4 *>(rowp);
+        // ---------------- all 2S steps, W steps per unrolled body (register renaming of the ring)
+#pragma unroll 1
+        for (int body = 0; body < STEPS / W; body++) {
+            unroll<W>([&](auto ic) {
+                constexpr int uu = decltype(ic)::value;
+                constexpr int su = uu % SPS;
+                if constexpr (su == 0) {
+                    mbar_wait(&full[gst % NSTAGE], (uint32_t)((gst / NSTAGE) & 1));
+                    __syncwarp();
+                }
+                const float4 *row4 = reinterpret_cast<const float4 *>(
+                    stagebuf + (gst % NSTAGE) * G::STAGEB + (UP ? su : (SPS - 1 - su)) * G::ROWB);
                 float acc[GRAD ? W : 1];
 #pragma unroll
                 for (int pp = 0; pp < W / 2; pp++) {
@@ -580,22 +635,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                     }
                 }
                 if constexpr (GRAD) {
-                    // reduce over the Lc column groups of this warp, then hand the warp's
-                    // per-slot sums to the CTA-level reduction through shared memory
 #pragma unroll
-                    for (int q = 0; q < W; q++)
+                    for (int q = 0; q < W; q++) {
+#pragma unroll
                         for (int o = L; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
-                    const int rbuf = (int)(gstep % kNRB);
-                    if (gstep >= kNRB) mbar_wait(&rempty[rbuf], (uint32_t)(((gstep - kNRB) / kNRB) & 1));
+                    }
+                    constexpr int d = uu % D;  // == gstep % D (W and STEPS are multiples of D)
+                    if (gstep >= D) mbar_wait(&rempty[d], (uint32_t)(((gstep - D) / D) & 1));
+                    __syncwarp();
                     if (g == 0) {
-                        float4 *dstp = reinterpret_cast<float4 *>(red + ((size_t)rbuf * kNW + warp) * S);
+                        float4 *dst = red + ((size_t)warp * D + d) * NCH;
 #pragma unroll
                         for (int q4 = 0; q4 < W / 4; q4++)
-                            dstp[q4 * L + t] = make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]);
+                            dst[q4 * L + t] = make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]);
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&rfull[rbuf]);
-                    if (gstep >= 1) reduce_step(gstep - 1);
+                    if (lane == 0) mbar_arrive(&rfull[d]);
+                    if (gstep >= LAG) reduce_step(gstep - LAG);
                     gstep++;
                 }
                 // ring shift to the next block's layout (Fig. 1)
@@ -608,24 +664,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                         shift_down<W>(ZT[p], ZB[p], first, last, L);
                     }
                 }
-                if (su == sps - 1) {
+                if constexpr (su == SPS - 1) {
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[gstage % kNStage]);
+                    if (lane == 0) mbar_arrive(&empty[gst % NSTAGE]);
                     if (threadIdx.x == 0) {
-                        int64_t nxt = gstage + kNStage - 1;
+                        const int nxt = gst + NSTAGE - 1;
                         if (nxt < total_stages) {
-                            int b = (int)(nxt % kNStage);
-                            if (nxt >= kNStage) mbar_wait(&empty[b], (uint32_t)(((nxt - kNStage) / kNStage) & 1));
-                            mbar_expect_tx(&full[b], stage_bytes);
-                            bulk_g2s(stagebuf + (size_t)b * stage_bytes, stage_src(nxt), stage_bytes, &full[b]);
+                            const int b = nxt % NSTAGE;
+                            if (nxt >= NSTAGE) mbar_wait(&empty[b], (uint32_t)(((nxt - NSTAGE) / NSTAGE) & 1));
+                            mbar_expect_tx(&full[b], G::STAGEB);
+                            bulk_g2s(stagebuf + (size_t)b * G::STAGEB, stage_src(nxt), G::STAGEB, &full[b]);
                         }
                     }
-                    gstage++;
+                    __syncwarp();
+                    gst++;
                 }
-            }
+            });
         }
 
-        // ---------------- store from the end layout
+        // ---------------- store from the end layout (s_{R-1} forward, s_0 backward)
         if (MODE == M_BWD && a.Y == nullptr) continue;
 #pragma unroll
         for (int q = 0; q < W; q++) {
@@ -641,7 +698,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                 else { vt[p] = ZT[p][q]; vb[p] = ZB[p][q]; }
             }
             if (!UP) {
-                bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }
@@ -650,7 +707,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
         }
     }
     if constexpr (GRAD) {
-        if (gstep >= 1) reduce_step(gstep - 1);
+        for (int gs = total_steps - LAG; gs < total_steps; gs++)
+            if (gs >= 0) reduce_step(gs);
+        if (lane == 0) bulk_wait_all();
     }
 }
 
@@ -789,10 +848,11 @@ namespace {
 
 using namespace gk;
 
-template <int W, int MODE>
-int launch_ring_w(const Cfg &c, RingArgs &ra, int64_t grid, cudaStream_t st) {
-    size_t smem = ring_smem_bytes(c, MODE);
-    auto kfn = k_ring<W, MODE>;
+template <int W, int L, int MODE>
+int launch_ring_wl(RingArgs &ra, int64_t grid, cudaStream_t st) {
+    constexpr size_t smem = RingGeom<W, L, MODE>::SMEM;
+    static_assert(smem <= 227 * 1024, "shared memory budget");
+    auto kfn = k_ring<W, L, MODE>;
     CUDA_TRY(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kfn<<<(unsigned)grid, kThreads, smem, st>>>(ra);
     CUDA_TRY(cudaGetLastError());
@@ -801,13 +861,24 @@ int launch_ring_w(const Cfg &c, RingArgs &ra, int64_t grid, cudaStream_t st) {
 
 template <int MODE>
 int launch_ring(const Cfg &c, RingArgs &ra, int64_t grid, cudaStream_t st) {
-    switch (c.W) {
-        case 4: return launch_ring_w<4, MODE>(c, ra, grid, st);
-        case 8: return launch_ring_w<8, MODE>(c, ra, grid, st);
-        case 16: return launch_ring_w<16, MODE>(c, ra, grid, st);
-        case 32: return launch_ring_w<32, MODE>(c, ra, grid, st);
+    if (c.L == 1) {
+        switch (c.W) {
+            case 4: return launch_ring_wl<4, 1, MODE>(ra, grid, st);
+            case 8: return launch_ring_wl<8, 1, MODE>(ra, grid, st);
+            case 16: return launch_ring_wl<16, 1, MODE>(ra, grid, st);
+            case 32: return launch_ring_wl<32, 1, MODE>(ra, grid, st);
+        }
+    } else if (c.W == 16) {
+        switch (c.L) {
+            case 4: return launch_ring_wl<16, 4, MODE>(ra, grid, st);
+            case 8: return launch_ring_wl<16, 8, MODE>(ra, grid, st);
+            case 16: return launch_ring_wl<16, 16, MODE>(ra, grid, st);
+            case 32: return launch_ring_wl<16, 32, MODE>(ra, grid, st);
+        }
+    } else if (c.W == 32 && c.L == 32) {
+        return launch_ring_wl<32, 32, MODE>(ra, grid, st);
     }
-    return fail(GIVENS_EUNSUPPORTED, "no ring kernel for W=%d", c.W);
+    return fail(GIVENS_EUNSUPPORTED, "no ring kernel for W=%d L=%d", c.W, c.L);
 }
 
 int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask, uint8_t *ws, const WsLayout &L,
@@ -852,7 +923,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
     int64_t grid = grid_for(c, mode, m);
     if (c.fast) {
         RingArgs ra;
-        ra.n = n; ra.ne = c.ne; ra.S = c.S; ra.L = c.L; ra.rowbytes = c.rowbytes; ra.sps = c.sps;
+        ra.n = n; ra.ne = c.ne;
         ra.m = m; ra.X = X; ra.ldx = ldx; ra.dY = dY; ra.lddy = lddy; ra.Y = Y; ra.ldy = ldy;
         ra.coef = ws + L.coef; ra.sfin = ws + L.sfin;
         ra.partial = reinterpret_cast<float *>(ws + L.partial);
@@ -984,7 +1055,7 @@ int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     int64_t G = grid_for(c, M_BWD, m);
     int64_t tot = (int64_t)2 * c.S * c.S;
     k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        c.S, (int)G, reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
+        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
         dtheta);
     CUDA_TRY(cudaGetLastError());
     return 0;
