@@ -56,7 +56,6 @@ def parse():
     ap.add_argument("--m", type=int, default=M_TOTAL)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample-cols", type=int, default=1024)
     ap.add_argument("--ref-cols-per-step", type=int, default=128)
     return ap.parse_args()
 
@@ -146,21 +145,30 @@ def run_reference(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(args):
+def cpu_baseline(args, target_s: float = 12.0):
+    """The fp64 oracle, as it stands, on the host cores, on a bounded column sample of the same
+    workload: a 128-column probe sizes the sample to ~target_s seconds of CPU work."""
     import numpy as np
 
     import oracle
     import synth
     n = args.n
     N = n * (n - 1) // 2
-    cols = args.cpu_sample_cols
     th = synth.theta(N, seed=SEED)
-    X = synth.normal_matrix(n, args.m, SEED, synth.TID_X, 0, cols).astype(np.float64)
-    dY = synth.normal_matrix(n, args.m, SEED, synth.TID_DY, 0, cols).astype(np.float64)
-    t0 = time.perf_counter()
-    oracle.apply(n, th, X)
-    oracle.backward(n, th, X, dY)
-    t = time.perf_counter() - t0
+
+    def run(cols):
+        X = synth.normal_matrix(n, args.m, SEED, synth.TID_X, 0, cols).astype(np.float64)
+        dY = synth.normal_matrix(n, args.m, SEED, synth.TID_DY, 0, cols).astype(np.float64)
+        t0 = time.perf_counter()
+        oracle.apply(n, th, X)
+        oracle.backward(n, th, X, dY)
+        return time.perf_counter() - t0
+
+    probe = 128
+    tp = run(probe)
+    cols = int(min(args.m, max(probe, probe * target_s / max(tp, 1e-3))))
+    cols = max(probe, cols // 64 * 64)
+    t = run(cols)
     return {"value": N * cols / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"first {cols} of {args.m} columns (n={n}): fp64 Alg. 1 forward + taped backward, "
                       f"{t:.1f} s wall"}

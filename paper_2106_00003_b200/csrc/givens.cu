@@ -425,26 +425,36 @@ struct RingGeom {
     static constexpr int STEPS = 2 * S;             // pad + the R = 2S-1 blocks
     static constexpr int LC = 32 / L;               // column groups per warp
     static constexpr int K = kcols(W, MODE);        // columns per thread
-    static constexpr int SPS = (W >= 32) ? 4 : W / 2;   // table rows per TMA stage (divides W)
+    // table rows per TMA stage: a power of two dividing W/2 with a stage of at most 16 KB
+    static constexpr int SPS = (W / 2 * S * 8 <= 16384) ? W / 2
+                             : (W / 4 * S * 8 <= 16384) ? W / 4
+                             : (W / 8 * S * 8 <= 16384) ? W / 8 : 1;
     static constexpr int ROWB = S * 8;              // bytes per table row
     static constexpr int STAGEB = SPS * ROWB;
-    static constexpr int NSTAGE = (S >= 1024) ? 2 : 3;
-    static constexpr int D = 4;                     // dtheta step ring depth (divides W)
-    static constexpr int LAG = 2;                   // a step is reduced LAG steps after it is written
+    static constexpr bool GRAD = (MODE == M_BWD);
+    // stages in flight: 64 KB of table buffers next to the backward's dtheta ring, 96 KB otherwise
+    static constexpr int NSTAGE_ = (GRAD ? 65536 : 98304) / STAGEB;
+    static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
+    // backward dtheta sums: per-warp ring of NG groups of RG steps, reduced one group later
+    static constexpr int RG = (S >= 1024) ? 2 : 4;  // steps per reduction group (divides W)
+    static constexpr int NG = 2;                    // groups in flight
+    static constexpr int D = RG * NG;               // ring depth in steps
     static constexpr int NCH = S / 4;               // float4 chunks of a step's per-slot sums
     static constexpr int OUTCH = (NCH + kNW - 1) / kNW;  // chunks reduced per warp (max)
-    static constexpr bool GRAD = (MODE == M_BWD);
     static constexpr size_t OFF_STAGE = 256;
     static constexpr size_t OFF_RED = OFF_STAGE + (size_t)NSTAGE * STAGEB;
     static constexpr size_t OFF_OUT = OFF_RED + (GRAD ? (size_t)kNW * D * NCH * 16 : 0);
-    static constexpr size_t SMEM = OFF_OUT + (GRAD ? (size_t)kNW * D * OUTCH * 16 : 0);
+    static constexpr size_t SMEM_ = OFF_OUT + (GRAD ? (size_t)kNW * D * OUTCH * 16 : 0);
+    static constexpr size_t SMEM = SMEM_;
 };
 
 // Hot-path kernel. One CTA of kNW warps owns a slab of C = kNW * LC * K columns; every column
 // lives in the registers of L lanes (ring.cuh). All 2S steps (pad + the n_eff-1 blocks) run
 // on-chip; the coefficient table streams through shared memory in TMA bulk stages; the
-// backward's per-slot column sums are reduced across warps LAG steps later and leave the SM
-// as TMA bulk reduce-adds into this CTA's private partial row (fixed order => deterministic).
+// backward's per-slot column sums go to a per-warp shared-memory ring in groups of RG steps; a
+// group is reduced across the warps one group later (each warp owns a chunk range) and leaves
+// the SM as TMA bulk reduce-adds into this CTA's private partial rows (fixed order, no
+// atomics => deterministic).
 template <int W, int L, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
     using G = RingGeom<W, L, MODE>;
@@ -453,19 +463,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
     constexpr int KP = IO::KP;
     constexpr int K = G::K;
     constexpr int S = G::S, STEPS = G::STEPS, LC = G::LC, SPS = G::SPS, NSTAGE = G::NSTAGE;
-    constexpr int D = G::D, LAG = G::LAG, NCH = G::NCH, OUTCH = G::OUTCH;
+    constexpr int RG = G::RG, NG = G::NG, D = G::D, NCH = G::NCH, OUTCH = G::OUTCH;
     constexpr bool UP = (MODE == M_TRANS || MODE == M_BWD);  // walk b_1 -> b_R (inverse rotations)
     constexpr bool GRAD = G::GRAD;
-    static_assert(W % SPS == 0 && W % D == 0 && W % 4 == 0, "geometry");
+    static_assert(W % SPS == 0 && W % RG == 0 && W % 4 == 0, "geometry");
 
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
-    uint64_t *empty = full + NSTAGE;
-    uint64_t *rfull = empty + NSTAGE;
-    uint64_t *rempty = rfull + D;
+    uint32_t *released = reinterpret_cast<uint32_t *>(full + NSTAGE);  // per-buffer warp release counts
+    uint64_t *rfull = full + NSTAGE + (NSTAGE + 1) / 2;
+    uint64_t *rempty = rfull + NG;
     uint8_t *stagebuf = smem + G::OFF_STAGE;
     float4 *red = reinterpret_cast<float4 *>(smem + G::OFF_RED);   // [kNW][D][NCH]
-    float4 *outb = reinterpret_cast<float4 *>(smem + G::OFF_OUT);  // [kNW][D][OUTCH]
+    float4 *outb = reinterpret_cast<float4 *>(smem + G::OFF_OUT);  // [kNW][NG][RG][OUTCH]
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int g = lane / L, t = lane % L;
@@ -481,9 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
     if (threadIdx.x == 0) {
         for (int i = 0; i < NSTAGE; i++) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kNW);
+            released[i] = 0;
         }
-        for (int i = 0; i < D; i++) {
+        for (int i = 0; i < NG; i++) {
             mbar_init(&rfull[i], kNW);
             mbar_init(&rempty[i], kNW);
         }
@@ -491,6 +501,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
         fence_proxy_async_smem();
     }
     __syncthreads();
+    if constexpr (GRAD) {
+        // pre-arm: every ring group starts out "empty" (phase 0 completes here), so the first
+        // use of each group waits on parity 0 without a special case
+        if (lane == 0)
+            for (int i = 0; i < NG; i++) mbar_arrive(&rempty[i]);
+    }
 
     // table rows of slab-local stage j: forward reads rho = 2S - u (descending), backward rho = u
     auto stage_src = [&](int gst) -> const uint8_t * {
@@ -499,50 +515,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
         return a.coef + (int64_t)rho0 * G::ROWB;
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NSTAGE - 1 && s < total_stages; s++) {
+        for (int s = 0; s < NSTAGE && s < total_stages; s++) {
             mbar_expect_tx(&full[s], G::STAGEB);
             bulk_g2s(stagebuf + (size_t)s * G::STAGEB, stage_src(s), G::STAGEB, &full[s]);
         }
     }
 
-    // dtheta stage 1: reduce global step gs (its per-warp sums sit in ring slot gs % D) over the
-    // kNW warps for this warp's chunk range and push it to this CTA's partial row.
-    auto reduce_step = [&](int gs) {
-        const int d = gs % D;
-        mbar_wait(&rfull[d], (uint32_t)((gs / D) & 1));
+    // dtheta stage 1: reduce ring group gg (steps gg*RG .. gg*RG+RG-1 of this CTA) over the kNW
+    // warps for this warp's chunk range and push it to this CTA's partial rows.
+    auto reduce_group = [&](int gg) {
+        const int bi = gg % NG;
+        mbar_wait(&rfull[bi], (uint32_t)((gg / NG) & 1));
+        if (lane == 0) bulk_wait_read<NG - 1>();  // the bulk ops that last read outb[bi] are done
         __syncwarp();
-        const int rho = gs % STEPS;
-        const bool first_slab = gs < STEPS;
-        float4 *ob = outb + ((size_t)warp * D + d) * OUTCH;
-        if (lane == 0) bulk_wait_read<D - 1>();   // the bulk op that last read ob has finished
-        __syncwarp();
-        const int ci = ch0 + lane;
-        if (ci < ch1) {
-            float4 s = red[((size_t)0 * D + d) * NCH + ci];
+        const int nch = ch1 - ch0;
+        float4 *ob = outb + ((size_t)warp * NG + bi) * RG * OUTCH;
+        for (int it = lane; it < RG * nch; it += 32) {
+            const int r = it / nch, c = it - r * nch;
+            const float4 *src = red + (size_t)(bi * RG + r) * NCH + ch0 + c;
+            float2 lo = make_float2(src[0].x, src[0].y), hi = make_float2(src[0].z, src[0].w);
 #pragma unroll
             for (int w = 1; w < kNW; w++) {
-                float4 v = red[((size_t)w * D + d) * NCH + ci];
-                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+                const float4 v = src[(size_t)w * D * NCH];
+                lo = __fadd2_rn(lo, make_float2(v.x, v.y));
+                hi = __fadd2_rn(hi, make_float2(v.z, v.w));
             }
-            ob[lane] = s;
+            ob[r * OUTCH + c] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
         __syncwarp();
         if (lane == 0) {
-            mbar_arrive(&rempty[d]);
-            if (ch1 > ch0) {
+            mbar_arrive(&rempty[bi]);
+            if (nch > 0) {
                 fence_proxy_async_smem();
-                float *dst = a.partial + ((int64_t)blockIdx.x * STEPS + rho) * S + ch0 * 4;
-                if (first_slab) bulk_s2g_store(dst, ob, (uint32_t)(ch1 - ch0) * 16);
-                else bulk_s2g_reduce_add(dst, ob, (uint32_t)(ch1 - ch0) * 16);
+                for (int r = 0; r < RG; r++) {
+                    const int gs = gg * RG + r;
+                    const int rho = gs % STEPS;
+                    float *dst = a.partial + ((int64_t)blockIdx.x * STEPS + rho) * S + ch0 * 4;
+                    if (gs < STEPS) bulk_s2g_store(dst, ob + r * OUTCH, (uint32_t)nch * 16);
+                    else bulk_s2g_reduce_add(dst, ob + r * OUTCH, (uint32_t)nch * 16);
+                }
                 bulk_commit();
-                // successive slabs add into the same partial row: keep them ordered
-                if (rho == STEPS - 1) bulk_wait_all();
+                // successive slabs add into the same partial rows: keep them ordered
+                if ((gg * RG + RG) % STEPS == 0) bulk_wait_all();
             }
         }
+        __syncwarp();
     };
 
     int gst = 0;    // coefficient stages consumed by this CTA
-    int gstep = 0;  // steps completed by this CTA
+    int grp = 0;    // dtheta ring groups completed by this CTA
     V ZT[KP][W], ZB[KP][W];
     V DT[GRAD ? KP : 1][GRAD ? W : 1], DB[GRAD ? KP : 1][GRAD ? W : 1];
 
@@ -603,7 +624,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                 }
                 const float4 *row4 = reinterpret_cast<const float4 *>(
                     stagebuf + (gst % NSTAGE) * G::STAGEB + (UP ? su : (SPS - 1 - su)) * G::ROWB);
-                float acc[GRAD ? W : 1];
+                constexpr int r = uu % RG;
+                int bi = 0;
+                float4 *ring_dst = nullptr;
+                if constexpr (GRAD) {
+                    bi = grp % NG;
+                    if constexpr (r == 0) {  // the ring group we are about to fill is free
+                        mbar_wait(&rempty[bi], (uint32_t)((grp / NG) & 1));
+                        __syncwarp();
+                    }
+                    ring_dst = red + ((size_t)warp * D + bi * RG + r) * NCH;
+                }
+                float acc[GRAD ? (LC > 1 ? W : 4) : 1];
 #pragma unroll
                 for (int pp = 0; pp < W / 2; pp++) {
                     const float4 cf = row4[pp * L + t];
@@ -614,14 +646,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                         if constexpr (GRAD) {
                             // dtheta contribution before this block's inverse rotation:
                             // dz_bottom * z_top - dz_top * z_bottom (Q_e structure)
-                            V s2 = mul_v(DB[0][q], ZT[0][q]);
-                            s2 = fma_v(neg_v(DT[0][q]), ZB[0][q], s2);
+                            float c = 0.f;
 #pragma unroll
-                            for (int p = 1; p < KP; p++) {
-                                s2 = fma_v(DB[p][q], ZT[p][q], s2);
-                                s2 = fma_v(neg_v(DT[p][q]), ZB[p][q], s2);
-                            }
-                            acc[q] = hsum(s2);
+                            for (int p = 0; p < KP; p++) c = cross_acc(c, DB[p][q], ZT[p][q], DT[p][q], ZB[p][q]);
+                            acc[LC > 1 ? q : (q & 3)] = c;
                         }
 #pragma unroll
                         for (int p = 0; p < KP; p++) {
@@ -633,26 +661,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                             }
                         }
                     }
+                    if constexpr (GRAD && LC == 1) {
+                        // one lane per column group: the per-slot sums go straight to the ring
+                        if (pp & 1) ring_dst[(pp >> 1) * L + t] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                    }
                 }
                 if constexpr (GRAD) {
+                    if constexpr (LC > 1) {
 #pragma unroll
-                    for (int q = 0; q < W; q++) {
+                        for (int q = 0; q < W; q++) {
 #pragma unroll
-                        for (int o = L; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                            for (int o = L; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                        }
+                        if (g == 0) {
+#pragma unroll
+                            for (int q4 = 0; q4 < W / 4; q4++)
+                                ring_dst[q4 * L + t] =
+                                    make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]);
+                        }
                     }
-                    constexpr int d = uu % D;  // == gstep % D (W and STEPS are multiples of D)
-                    if (gstep >= D) mbar_wait(&rempty[d], (uint32_t)(((gstep - D) / D) & 1));
-                    __syncwarp();
-                    if (g == 0) {
-                        float4 *dst = red + ((size_t)warp * D + d) * NCH;
-#pragma unroll
-                        for (int q4 = 0; q4 < W / 4; q4++)
-                            dst[q4 * L + t] = make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]);
+                    if constexpr (r == RG - 1) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&rfull[bi]);
+                        // warps w and w+4 share an SMSP: the low half reduces the previous group
+                        // here, the high half RG/2 steps later, so one of them keeps the FMA pipe busy
+                        if (warp < 4 && grp >= 1) reduce_group(grp - 1);
+                        grp++;
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&rfull[d]);
-                    if (gstep >= LAG) reduce_step(gstep - LAG);
-                    gstep++;
+                    if constexpr (r == RG / 2 - 1) {
+                        if (warp >= 4 && grp >= 1) reduce_group(grp - 1);
+                    }
                 }
                 // ring shift to the next block's layout (Fig. 1)
 #pragma unroll
@@ -665,15 +703,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                     }
                 }
                 if constexpr (su == SPS - 1) {
+                    // release the stage buffer; the LAST warp to release it refills it with the
+                    // stage NSTAGE ahead (no warp ever waits to act as the producer)
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[gst % NSTAGE]);
-                    if (threadIdx.x == 0) {
-                        const int nxt = gst + NSTAGE - 1;
-                        if (nxt < total_stages) {
-                            const int b = nxt % NSTAGE;
-                            if (nxt >= NSTAGE) mbar_wait(&empty[b], (uint32_t)(((nxt - NSTAGE) / NSTAGE) & 1));
-                            mbar_expect_tx(&full[b], G::STAGEB);
-                            bulk_g2s(stagebuf + (size_t)b * G::STAGEB, stage_src(nxt), G::STAGEB, &full[b]);
+                    if (lane == 0) {
+                        const int b = gst % NSTAGE;
+                        __threadfence_block();  // this warp's reads of buffer b happen-before the release
+                        if (atomicAdd(&released[b], 1u) == kNW - 1) {
+                            __threadfence_block();
+                            released[b] = 0;
+                            const int nxt = gst + NSTAGE;
+                            if (nxt < total_stages) {
+                                fence_proxy_async_smem();
+                                mbar_expect_tx(&full[b], G::STAGEB);
+                                bulk_g2s(stagebuf + (size_t)b * G::STAGEB, stage_src(nxt), G::STAGEB, &full[b]);
+                            }
                         }
                     }
                     __syncwarp();
@@ -707,10 +751,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
         }
     }
     if constexpr (GRAD) {
-        for (int gs = total_steps - LAG; gs < total_steps; gs++)
-            if (gs >= 0) reduce_step(gs);
+        if (grp >= 1) reduce_group(grp - 1);  // both halves: the last group is still pending
         if (lane == 0) bulk_wait_all();
     }
+    (void)total_steps;
 }
 
 // ------------------------------------------------------------------ generic any-n kernel

@@ -30,8 +30,17 @@ __device__ __forceinline__ float2 mul_v(float2 a, float2 b) { return __fmul2_rn(
 __device__ __forceinline__ float neg_v(float a) { return -a; }
 __device__ __forceinline__ float2 neg_v(float2 a) { return make_float2(-a.x, -a.y); }
 
-__device__ __forceinline__ float hsum(float a) { return a; }
-__device__ __forceinline__ float hsum(float2 a) { return a.x + a.y; }
+// acc += db*zt - dt*zb summed over the packed columns, in scalar FFMAs (4 pipe cycles per
+// packed pair instead of FMUL2 + FFMA2 + FADD = 5)
+__device__ __forceinline__ float cross_acc(float acc, float db, float zt, float dt, float zb) {
+    return fmaf(-dt, zb, fmaf(db, zt, acc));
+}
+__device__ __forceinline__ float cross_acc(float acc, float2 db, float2 zt, float2 dt, float2 zb) {
+    acc = fmaf(db.x, zt.x, acc);
+    acc = fmaf(db.y, zt.y, acc);
+    acc = fmaf(-dt.x, zb.x, acc);
+    return fmaf(-dt.y, zb.y, acc);
+}
 
 __device__ __forceinline__ float shfl_up_v(float v, int w) { return __shfl_up_sync(0xffffffffu, v, 1, w); }
 __device__ __forceinline__ float2 shfl_up_v(float2 v, int w) {
