@@ -11,15 +11,22 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-SRC = os.path.join(HERE, "csrc", "givens.cu")
-DEPS = [SRC, os.path.join(HERE, "csrc", "ring.cuh"), os.path.join(ROOT, "include", "givens.h")]
+CSRC = os.path.join(HERE, "csrc")
+SRC = os.path.join(CSRC, "givens.cu")
+RING_SRC = os.path.join(CSRC, "ring_inst.cu")
+DEPS = [SRC, RING_SRC, os.path.join(CSRC, "ring.cuh"), os.path.join(CSRC, "common.cuh"),
+        os.path.join(ROOT, "include", "givens.h")]
 LIB = os.path.join(HERE, "libgivens.so")
+OBJ = os.path.join(HERE, "build_obj")
+# (W, L) ring configurations; must match GK_RING_CONFIGS in csrc/givens.cu
+RING_CONFIGS = [(4, 1), (8, 1), (16, 1), (32, 1), (16, 4), (16, 8), (16, 16), (16, 32), (8, 64), (16, 64),
+                (32, 32), (16, 128)]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-diag-suppress", "177",
 ]
 
@@ -32,13 +39,28 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [NVCC, *FLAGS, "-o", tmp, SRC]
+    """Compile every translation unit (the ring configurations in parallel) and link the .so."""
+    if not (force or needs_build()):
+        return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ, exist_ok=True)
+    jobs = [([NVCC, *FLAGS, "-c", "-o", os.path.join(OBJ, "givens.o"), SRC], "givens.o")]
+    for w, l in RING_CONFIGS:
+        o = os.path.join(OBJ, f"ring_{w}_{l}.o")
+        jobs.append(([NVCC, *FLAGS, f"-DRING_W={w}", f"-DRING_L={l}", "-c", "-o", o, RING_SRC], o))
+
+    def run(job):
+        cmd, _ = job
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        list(ex.map(run, jobs))
+    objs = [os.path.join(OBJ, "givens.o")] + [os.path.join(OBJ, f"ring_{w}_{l}.o") for w, l in RING_CONFIGS]
+    tmp = LIB + f".tmp{os.getpid()}"
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
+    os.replace(tmp, LIB)
     return LIB
 
 

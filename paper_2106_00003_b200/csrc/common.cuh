@@ -1,0 +1,663 @@
+// common.cuh -- device-side pieces shared by the C-ABI translation unit (givens.cu) and the
+// per-configuration ring-kernel instantiations (ring_inst.cu): the closed-form schedule, PTX
+// helpers (mbarrier, TMA bulk copies), and the register-ring kernel template k_ring<W,L,MODE>.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+#include <utility>
+
+#include "ring.cuh"
+
+namespace gk {
+
+// ------------------------------------------------------------------ schedule (closed form)
+// Circle method (Fig. 1): s_r[0] = 0, s_r[p] = 1 + ((p-1-r) mod (n_eff-1));
+// block b_{r+1} pairs positions k and n_eff-1-k. Odd n: bye index n sits at
+// position r (r >= 1) or n_eff-1 (r = 0), i.e. in slot 0 at r = 0 and min(r, n_eff-1-r) else.
+__host__ __device__ inline int seq_at(int r, int p, int ne) {
+    int R = ne - 1;
+    if (p == 0) return 0;
+    int v = (p - 1 - r) % R;
+    if (v < 0) v += R;
+    return 1 + v;
+}
+__host__ __device__ inline int bye_slot(int r, int ne) {
+    if (r == 0) return 0;
+    return r < ne - 1 - r ? r : ne - 1 - r;
+}
+// flat angle index of (block r, slot k) in block-major order skipping byes; -1 for the bye.
+__host__ __device__ inline int64_t flat_of(int r, int k, int n, int ne) {
+    int S = ne / 2;
+    if (n == ne) return (int64_t)r * S + k;
+    int kb = bye_slot(r, ne);
+    if (k == kb) return -1;
+    return (int64_t)r * (S - 1) + k - (k > kb ? 1 : 0);
+}
+// position of row i in s_r
+__host__ __device__ inline int pos_of(int i, int r, int ne) {
+    if (i == 0) return 0;
+    int R = ne - 1;
+    return 1 + ((i - 1 + r) % R);
+}
+
+constexpr int kNW = 8;           // warps per CTA of the ring kernel
+constexpr int kThreads = kNW * 32;
+
+enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3 };
+
+__host__ __device__ constexpr int kcols(int W, int mode) {
+    // columns per thread, so that the column state is ~128 registers (2 W K forward, 4 W K
+    // backward); two packed fp32 columns per FFMA2
+    return (mode == M_BWD) ? (32 / W > 8 ? 8 : 32 / W) : (64 / W > 8 ? 8 : 64 / W);
+}
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *b, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t *b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// structured (C++-level) spin so the compiler sees the loop and re-converges the warp after it
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+    while (!mbar_try(b, parity)) {
+    }
+}
+
+// compile-time unrolling: f(std::integral_constant<int, I>{}) for I = 0..N-1, as straight-line code
+template <typename F, int... I>
+__device__ __forceinline__ void unroll_impl(F &&f, std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void unroll(F &&f) {
+    unroll_impl(f, std::make_integer_sequence<int, N>{});
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// ------------------------------------------------------------------ the register-ring kernel
+struct RingArgs {
+    int n, ne;
+    int64_t m;
+    const float *X;   // FWD/TRANS: input; BWD: Y
+    int64_t ldx;
+    const float *dY;  // BWD only
+    int64_t lddy;
+    float *Y;         // FWD/BUILDU/TRANS: output; BWD: dX (nullable)
+    int64_t ldy;
+    const uint8_t *coef;
+    const uint8_t *sfin;
+    float *partial;   // BWD: [grid][2S][S] in chunk order (see chunk_pos)
+    int64_t nslabs;
+    int vec_ok;       // 1 if all row starts are 16-byte aligned for K-wide vector access
+};
+
+template <int K>
+struct ColIO;
+template <>
+struct ColIO<1> {
+    using V = float;
+    static constexpr int KP = 1;
+    __device__ static void load(const float *row, int64_t c0, int64_t m, int, V (&v)[1]) {
+        v[0] = c0 < m ? __ldg(row + c0) : 0.f;
+    }
+    __device__ static void store(float *row, int64_t c0, int64_t m, int, const V (&v)[1]) {
+        if (c0 < m) row[c0] = v[0];
+    }
+};
+template <>
+struct ColIO<2> {
+    using V = float2;
+    static constexpr int KP = 1;
+    __device__ static void load(const float *row, int64_t c0, int64_t m, int vec, V (&v)[1]) {
+        if (vec && c0 + 2 <= m) {
+            v[0] = __ldg(reinterpret_cast<const float2 *>(row + c0));
+        } else {
+            v[0].x = c0 < m ? __ldg(row + c0) : 0.f;
+            v[0].y = c0 + 1 < m ? __ldg(row + c0 + 1) : 0.f;
+        }
+    }
+    __device__ static void store(float *row, int64_t c0, int64_t m, int vec, const V (&v)[1]) {
+        if (vec && c0 + 2 <= m) {
+            *reinterpret_cast<float2 *>(row + c0) = v[0];
+        } else {
+            if (c0 < m) row[c0] = v[0].x;
+            if (c0 + 1 < m) row[c0 + 1] = v[0].y;
+        }
+    }
+};
+template <>
+struct ColIO<4> {
+    using V = float2;
+    static constexpr int KP = 2;
+    __device__ static void load(const float *row, int64_t c0, int64_t m, int vec, V (&v)[2]) {
+        if (vec && c0 + 4 <= m) {
+            float4 a = __ldg(reinterpret_cast<const float4 *>(row + c0));
+            v[0] = make_float2(a.x, a.y);
+            v[1] = make_float2(a.z, a.w);
+        } else {
+            v[0].x = c0 < m ? __ldg(row + c0) : 0.f;
+            v[0].y = c0 + 1 < m ? __ldg(row + c0 + 1) : 0.f;
+            v[1].x = c0 + 2 < m ? __ldg(row + c0 + 2) : 0.f;
+            v[1].y = c0 + 3 < m ? __ldg(row + c0 + 3) : 0.f;
+        }
+    }
+    __device__ static void store(float *row, int64_t c0, int64_t m, int vec, const V (&v)[2]) {
+        if (vec && c0 + 4 <= m) {
+            *reinterpret_cast<float4 *>(row + c0) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+        } else {
+            if (c0 < m) row[c0] = v[0].x;
+            if (c0 + 1 < m) row[c0 + 1] = v[0].y;
+            if (c0 + 2 < m) row[c0 + 2] = v[1].x;
+            if (c0 + 3 < m) row[c0 + 3] = v[1].y;
+        }
+    }
+};
+
+template <>
+struct ColIO<8> {
+    using V = float2;
+    static constexpr int KP = 4;
+    __device__ static void load(const float *row, int64_t c0, int64_t m, int vec, V (&v)[4]) {
+        if (vec && c0 + 8 <= m) {
+            float4 a = __ldg(reinterpret_cast<const float4 *>(row + c0));
+            float4 b = __ldg(reinterpret_cast<const float4 *>(row + c0 + 4));
+            v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
+            v[2] = make_float2(b.x, b.y); v[3] = make_float2(b.z, b.w);
+        } else {
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+                v[p].x = c0 + 2 * p < m ? __ldg(row + c0 + 2 * p) : 0.f;
+                v[p].y = c0 + 2 * p + 1 < m ? __ldg(row + c0 + 2 * p + 1) : 0.f;
+            }
+        }
+    }
+    __device__ static void store(float *row, int64_t c0, int64_t m, int vec, const V (&v)[4]) {
+        if (vec && c0 + 8 <= m) {
+            *reinterpret_cast<float4 *>(row + c0) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+            *reinterpret_cast<float4 *>(row + c0 + 4) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+        } else {
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+                if (c0 + 2 * p < m) row[c0 + 2 * p] = v[p].x;
+                if (c0 + 2 * p + 1 < m) row[c0 + 2 * p + 1] = v[p].y;
+            }
+        }
+    }
+};
+
+template <typename V>
+__device__ __forceinline__ V vneg_if(V v, bool neg) { return neg ? neg_v(v) : v; }
+
+__device__ __forceinline__ void bulk_s2g_reduce_add(float *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_store(float *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Compile-time geometry of one ring configuration: W slots per lane, L lanes per column group
+// (L < 32: several groups per warp; L = 32 H: a group spans H warps).
+template <int W, int L, int MODE>
+struct RingGeom {
+    static constexpr int S = W * L;                 // slots = n_eff / 2
+    static constexpr int STEPS = 2 * S;             // pad + the R = 2S-1 blocks
+    static constexpr int LW = L < 32 ? L : 32;      // lanes of a group inside one warp
+    static constexpr int H = L / LW;                // warps per column group
+    static constexpr int LC = 32 / LW;              // column groups per warp
+    static constexpr int NGRP = kNW * LC / H;       // column groups per CTA
+    static constexpr int K = kcols(W, MODE);        // columns per thread
+    static constexpr bool GRAD = (MODE == M_BWD);
+    static constexpr int KP = (K + 1) / 2;          // packed register pairs per slot
+    // table rows per TMA stage: a power of two dividing W/2 with a stage of at most 16 KB
+    static constexpr int sps_pick() {
+        int v = W / 2;
+        while (v > 1 && v * S * 8 > 16384) v /= 2;
+        return v;
+    }
+    static constexpr int SPS = sps_pick();
+    static constexpr int ROWB = S * 8;              // bytes per table row
+    static constexpr int STAGEB = SPS * ROWB;
+    // stages in flight: 64 KB of table buffers next to the backward's dtheta ring, 96 KB otherwise
+    static constexpr int NSTAGE_ = (GRAD ? 65536 : 98304) / STAGEB;
+    static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
+    // backward dtheta sums: per-warp ring of NG groups of RG steps, reduced one group later
+    static constexpr int RG = ((W / 4) * LW >= 256 || (H > 1 && (W / 4) * LW >= 128)) ? 2 : 4;  // steps per group
+    static constexpr int NG = 2;                    // groups in flight
+    static constexpr int D = RG * NG;               // ring depth in steps
+    static constexpr int NCH = S / 4;               // float4 chunks of a step's per-slot sums
+    static constexpr int NCHW = (W / 4) * LW;       // chunks held by one warp (= NCH / H)
+    static constexpr int NSUM = kNW / H;            // warps contributing to each chunk
+    static constexpr int OUTCH = (NCHW + NSUM - 1) / NSUM;  // chunks reduced per warp (max)
+    static constexpr int XV = GRAD ? 2 * KP : KP;   // packed values crossing a warp boundary per direction
+    static constexpr size_t OFF_STAGE = 256;
+    static constexpr size_t OFF_X = OFF_STAGE + (size_t)NSTAGE * STAGEB;
+    static constexpr size_t OFF_RED = OFF_X + (H > 1 ? (size_t)2 * kNW * 2 * XV * 8 : 0);
+    static constexpr size_t OFF_OUT = OFF_RED + (GRAD ? (size_t)kNW * D * NCHW * 16 : 0);
+    static constexpr size_t SMEM = OFF_OUT + (GRAD ? (size_t)kNW * NG * RG * OUTCH * 16 : 0);
+};
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Hot-path kernel. One CTA of kNW warps owns a slab of C = NGRP * K columns; every column
+// lives in the registers of L lanes (ring.cuh). All 2S steps (pad + the n_eff-1 blocks) run
+// on-chip; the coefficient table streams through shared memory in TMA bulk stages; values that
+// cross a warp boundary of a multi-warp column group go through shared memory under a named
+// barrier; the backward's per-slot column sums go to a per-warp shared-memory ring in groups of
+// RG steps, are reduced across the warps holding the same slots one group later (each warp owns
+// a chunk range) and leave the SM as TMA bulk reduce-adds into this CTA's private partial rows
+// (fixed order, no atomics => deterministic).
+template <int W, int L, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
+    using G = RingGeom<W, L, MODE>;
+    using IO = ColIO<G::K>;
+    using V = typename IO::V;
+    constexpr int KP = IO::KP;
+    constexpr int K = G::K;
+    constexpr int S = G::S, STEPS = G::STEPS, LW = G::LW, H = G::H, LC = G::LC, SPS = G::SPS,
+                  NSTAGE = G::NSTAGE;
+    constexpr int RG = G::RG, NG = G::NG, D = G::D, NCHW = G::NCHW, NSUM = G::NSUM, OUTCH = G::OUTCH;
+    constexpr int XV = G::XV;
+    constexpr bool UP = (MODE == M_TRANS || MODE == M_BWD);  // walk b_1 -> b_R (inverse rotations)
+    constexpr bool GRAD = G::GRAD;
+    static_assert(W % SPS == 0 && W % RG == 0 && W % 4 == 0 && W % 2 == 0, "geometry");
+    static_assert(H == 1 || LW == 32, "multi-warp groups use whole warps");
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem);
+    uint32_t *released = reinterpret_cast<uint32_t *>(full + NSTAGE);  // per-buffer warp release counts
+    uint64_t *rfull = full + NSTAGE + (NSTAGE + 1) / 2;
+    uint64_t *rempty = rfull + NG;
+    uint8_t *stagebuf = smem + G::OFF_STAGE;
+    V *xbuf = reinterpret_cast<V *>(smem + G::OFF_X);                 // [2][kNW][2][XV]
+    float4 *red = reinterpret_cast<float4 *>(smem + G::OFF_RED);   // [kNW][D][NCHW]
+    float4 *outb = reinterpret_cast<float4 *>(smem + G::OFF_OUT);  // [kNW][NG][RG][OUTCH]
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int h = warp % H;                       // which warp of its column group
+    const int cw = warp / H;                      // warp-group index in the CTA
+    const int g = lane / LW;                      // column group inside the warp (LC > 1)
+    const int tl = lane % LW;                     // lane inside the group's warp slice
+    const int t = h * LW + tl;                    // lane inside the column group
+    const bool first = (t == 0), last = (t == L - 1);
+    const int ne = a.ne, n = a.n;
+    const int64_t C = (int64_t)G::NGRP * K;
+    const int my_slabs = (int)((a.nslabs - blockIdx.x + gridDim.x - 1) / gridDim.x);
+    const int total_stages = my_slabs * (STEPS / SPS);
+    // chunk range (of this warp's half h) of the per-step sums this warp reduces
+    const int ch0 = (cw * NCHW) / NSUM, ch1 = ((cw + 1) * NCHW) / NSUM;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < NSTAGE; i++) {
+            mbar_init(&full[i], 1);
+            released[i] = 0;
+        }
+        for (int i = 0; i < NG; i++) {
+            mbar_init(&rfull[i], kNW);
+            mbar_init(&rempty[i], kNW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async_smem();
+    }
+    __syncthreads();
+    if constexpr (GRAD) {
+        // pre-arm: every ring group starts out "empty" (phase 0 completes here), so the first
+        // use of each group waits on parity 0 without a special case
+        if (lane == 0)
+            for (int i = 0; i < NG; i++) mbar_arrive(&rempty[i]);
+    }
+
+    // table rows of slab-local stage j: forward reads rho = 2S - u (descending), backward rho = u
+    auto stage_src = [&](int gst) -> const uint8_t * {
+        int j = gst % (STEPS / SPS);
+        int rho0 = UP ? j * SPS : (STEPS - (j + 1) * SPS + 1);
+        return a.coef + (int64_t)rho0 * G::ROWB;
+    };
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NSTAGE && s < total_stages; s++) {
+            mbar_expect_tx(&full[s], G::STAGEB);
+            bulk_g2s(stagebuf + (size_t)s * G::STAGEB, stage_src(s), G::STAGEB, &full[s]);
+        }
+    }
+
+    // dtheta stage 1: reduce ring group gg (steps gg*RG .. gg*RG+RG-1 of this CTA) over the NSUM
+    // warps holding the same slots, for this warp's chunk range, and push it to the partial rows.
+    auto reduce_group = [&](int gg) {
+        const int bi = gg % NG;
+        mbar_wait(&rfull[bi], (uint32_t)((gg / NG) & 1));
+        if (lane == 0) bulk_wait_read<NG - 1>();  // the bulk ops that last read outb[bi] are done
+        __syncwarp();
+        float4 *ob = outb + ((size_t)warp * NG + bi) * RG * OUTCH;
+        const float4 *rsrc = red + ((size_t)h * D + bi * RG) * NCHW + ch0;  // warp h of group 0
+        constexpr bool EVEN = (NCHW % NSUM) == 0;  // every warp owns exactly OUTCH chunks
+        const int nch = EVEN ? OUTCH : ch1 - ch0;
+        auto sum_item = [&](int r, int c) {
+            const float4 *src = rsrc + (size_t)r * NCHW + c;
+            float2 lo = make_float2(src[0].x, src[0].y), hi = make_float2(src[0].z, src[0].w);
+#pragma unroll
+            for (int w = 1; w < NSUM; w++) {
+                const float4 v = src[(size_t)w * H * D * NCHW];
+                lo = __fadd2_rn(lo, make_float2(v.x, v.y));
+                hi = __fadd2_rn(hi, make_float2(v.z, v.w));
+            }
+            ob[r * OUTCH + c] = make_float4(lo.x, lo.y, hi.x, hi.y);
+        };
+        if constexpr (EVEN) {
+            constexpr int ITEMS = RG * OUTCH;
+#pragma unroll
+            for (int j = 0; j < (ITEMS + 31) / 32; j++) {
+                const int it = lane + 32 * j;
+                if (ITEMS % 32 == 0 || it < ITEMS) sum_item(it / OUTCH, it % OUTCH);
+            }
+        } else {
+            for (int it = lane; it < RG * nch; it += 32) sum_item(it / nch, it % nch);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&rempty[bi]);
+            if (nch > 0) {
+                fence_proxy_async_smem();
+                const int gs0 = gg * RG;
+                const int rho0 = gs0 % STEPS;
+                float *dst = a.partial + ((int64_t)blockIdx.x * STEPS + rho0) * S + (h * NCHW + ch0) * 4;
+#pragma unroll
+                for (int r = 0; r < RG; r++) {
+                    if (gs0 < STEPS) bulk_s2g_store(dst + (size_t)r * S, ob + r * OUTCH, (uint32_t)nch * 16);
+                    else bulk_s2g_reduce_add(dst + (size_t)r * S, ob + r * OUTCH, (uint32_t)nch * 16);
+                }
+                bulk_commit();
+                // successive slabs add into the same partial rows: keep them ordered
+                if (rho0 + RG == STEPS) bulk_wait_all();
+            }
+        }
+        __syncwarp();
+    };
+
+    int gst = 0;    // coefficient stages consumed by this CTA
+    int grp = 0;    // dtheta ring groups completed by this CTA
+    V ZT[KP][W], ZB[KP][W];
+    V DT[GRAD ? KP : 1][GRAD ? W : 1], DB[GRAD ? KP : 1][GRAD ? W : 1];
+
+    for (int64_t slab = blockIdx.x; slab < a.nslabs; slab += gridDim.x) {
+        const int64_t col0 = slab * C + (int64_t)(cw * LC + g) * K;
+        // ---------------- load the slab into the start layout (s_0 forward, s_{R-1} backward)
+#pragma unroll
+        for (int q = 0; q < W; q++) {
+            const int k = t * W + q;
+            const int pt = k, pb = ne - 1 - k;
+            int rt, rb;
+            if (UP) { rt = row_sRm1(pt, ne); rb = row_sRm1(pb, ne); }
+            else    { rt = row_s0(pt);       rb = row_s0(pb); }
+            V vt[KP], vb[KP];
+            if constexpr (MODE == M_BUILDU) {
+#pragma unroll
+                for (int p = 0; p < KP; p++) {
+                    const int64_t c = col0 + 2 * p;
+                    vt[p] = make_float2((rt < n && c == rt) ? 1.f : 0.f, (rt < n && c + 1 == rt) ? 1.f : 0.f);
+                    vb[p] = make_float2((rb < n && c == rb) ? 1.f : 0.f, (rb < n && c + 1 == rb) ? 1.f : 0.f);
+                }
+            } else {
+                if (rt < n) IO::load(a.X + (int64_t)rt * a.ldx, col0, a.m, a.vec_ok, vt);
+                else for (int p = 0; p < KP; p++) vt[p] = V{};
+                if (rb < n) IO::load(a.X + (int64_t)rb * a.ldx, col0, a.m, a.vec_ok, vb);
+                else for (int p = 0; p < KP; p++) vb[p] = V{};
+            }
+            if (UP) {
+                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+#pragma unroll
+                for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
+            }
+#pragma unroll
+            for (int p = 0; p < KP; p++) { ZT[p][q] = vt[p]; ZB[p][q] = vb[p]; }
+            if constexpr (GRAD) {
+                if (rt < n) IO::load(a.dY + (int64_t)rt * a.lddy, col0, a.m, a.vec_ok, vt);
+                else for (int p = 0; p < KP; p++) vt[p] = V{};
+                if (rb < n) IO::load(a.dY + (int64_t)rb * a.lddy, col0, a.m, a.vec_ok, vb);
+                else for (int p = 0; p < KP; p++) vb[p] = V{};
+                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+#pragma unroll
+                for (int p = 0; p < KP; p++) {
+                    DT[p][q] = vneg_if(vt[p], nt);
+                    DB[p][q] = vneg_if(vb[p], nb);
+                }
+            }
+        }
+
+        // ---------------- all 2S steps, W steps per unrolled body (register renaming of the ring)
+#pragma unroll 1
+        for (int body = 0; body < STEPS / W; body++) {
+            unroll<W>([&](auto ic) {
+                constexpr int uu = decltype(ic)::value;
+                constexpr int su = uu % SPS;
+                if constexpr (su == 0) {
+                    mbar_wait(&full[gst % NSTAGE], (uint32_t)((gst / NSTAGE) & 1));
+                    __syncwarp();
+                }
+                const float4 *row4 = reinterpret_cast<const float4 *>(
+                    stagebuf + (gst % NSTAGE) * G::STAGEB + (UP ? su : (SPS - 1 - su)) * G::ROWB);
+                constexpr int r = uu % RG;
+                int bi = 0;
+                float4 *ring_dst = nullptr;
+                if constexpr (GRAD) {
+                    bi = grp % NG;
+                    if constexpr (r == 0) {  // the ring group we are about to fill is free
+                        mbar_wait(&rempty[bi], (uint32_t)((grp / NG) & 1));
+                        __syncwarp();
+                    }
+                    ring_dst = red + ((size_t)warp * D + bi * RG + r) * NCHW;
+                }
+                float acc[GRAD ? (LC > 1 ? W : 4) : 1];
+#pragma unroll
+                for (int pp = 0; pp < W / 2; pp++) {
+                    const float4 cf = row4[pp * L + t];
+#pragma unroll
+                    for (int hh = 0; hh < 2; hh++) {
+                        const int q = 2 * pp + hh;
+                        const float tq = hh ? cf.z : cf.x, sq = hh ? cf.w : cf.y;
+                        if constexpr (GRAD) {
+                            // dtheta contribution before this block's inverse rotation:
+                            // dz_bottom * z_top - dz_top * z_bottom (Q_e structure)
+                            float c = 0.f;
+#pragma unroll
+                            for (int p = 0; p < KP; p++) c = cross_acc(c, DB[p][q], ZT[p][q], DT[p][q], ZB[p][q]);
+                            acc[LC > 1 ? q : (q & 3)] = c;
+                        }
+#pragma unroll
+                        for (int p = 0; p < KP; p++) {
+                            if (UP) {
+                                rot_inv(ZT[p][q], ZB[p][q], tq, sq);
+                                if constexpr (GRAD) rot_inv(DT[p][q], DB[p][q], tq, sq);
+                            } else {
+                                rot_fwd(ZT[p][q], ZB[p][q], tq, sq);
+                            }
+                        }
+                    }
+                    if constexpr (GRAD && LC == 1) {
+                        // one lane per column group and warp: the per-slot sums go straight to the ring
+                        if (pp & 1) ring_dst[(pp >> 1) * LW + tl] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                    }
+                }
+                if constexpr (GRAD) {
+                    if constexpr (LC > 1) {
+#pragma unroll
+                        for (int q = 0; q < W; q++) {
+#pragma unroll
+                            for (int o = LW; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                        }
+                        if (g == 0) {
+#pragma unroll
+                            for (int q4 = 0; q4 < W / 4; q4++)
+                                ring_dst[q4 * LW + tl] =
+                                    make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]);
+                        }
+                    }
+                    if constexpr (r == RG - 1) {
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&rfull[bi]);
+                        // warps w and w+4 share an SMSP: the low half reduces the previous group
+                        // here, the high half RG/2 steps earlier, so one of them keeps the FMA pipe busy
+                        if (warp < 4 && grp >= 1) reduce_group(grp - 1);
+                        grp++;
+                    }
+                    if constexpr (r == RG / 2 - 1) {
+                        if (warp >= 4 && grp >= 1) reduce_group(grp - 1);
+                    }
+                }
+                // ring shift to the next block's layout (Fig. 1)
+                if constexpr (H == 1) {
+#pragma unroll
+                    for (int p = 0; p < KP; p++) {
+                        if (UP) {
+                            shift_up<W>(ZT[p], ZB[p], first, last, L);
+                            if constexpr (GRAD) shift_up<W>(DT[p], DB[p], first, last, L);
+                        } else {
+                            shift_down<W>(ZT[p], ZB[p], first, last, L);
+                        }
+                    }
+                } else {
+                    // values crossing a warp boundary: publish, named barrier of the group, read
+                    constexpr int par = uu & 1;  // double buffer (W is even)
+                    V *xo = xbuf + ((size_t)(par * kNW + warp) * 2) * XV;  // [0]: to warp h-1, [1]: to warp h+1
+                    if (UP) {
+                        // lane t+1 needs my T[W-1] (from_prev), lane t-1 needs my B[0] (from_next)
+                        if (lane == 31) {
+#pragma unroll
+                            for (int p = 0; p < KP; p++) {
+                                xo[XV + p] = ZT[p][W - 1];
+                                if constexpr (GRAD) xo[XV + KP + p] = DT[p][W - 1];
+                            }
+                        }
+                        if (lane == 0) {
+#pragma unroll
+                            for (int p = 0; p < KP; p++) {
+                                xo[p] = ZB[p][0];
+                                if constexpr (GRAD) xo[KP + p] = DB[p][0];
+                            }
+                        }
+                    } else {
+                        // lane t-1 needs my T[0] (its from_next), lane t+1 needs my B[W-1] (its from_prev)
+                        if (lane == 0) {
+#pragma unroll
+                            for (int p = 0; p < KP; p++) xo[p] = ZT[p][0];
+                        }
+                        if (lane == 31) {
+#pragma unroll
+                            for (int p = 0; p < KP; p++) xo[XV + p] = ZB[p][W - 1];
+                        }
+                    }
+                    named_bar(1 + cw, 32 * H);
+                    const V *xprev = xbuf + ((size_t)(par * kNW + warp - 1) * 2) * XV;  // warp h-1 of my group
+                    const V *xnext = xbuf + ((size_t)(par * kNW + warp + 1) * 2) * XV;  // warp h+1
+                    const bool from_x_prev = (lane == 0 && h > 0), from_x_next = (lane == 31 && h < H - 1);
+#pragma unroll
+                    for (int p = 0; p < KP; p++) {
+                        if (UP) {
+                            V fp = shfl_up_v(ZT[p][W - 1], 32), fn = shfl_dn_v(ZB[p][0], 32);
+                            if (from_x_prev) fp = xprev[XV + p];
+                            if (from_x_next) fn = xnext[p];
+                            shift_up_with<W>(ZT[p], ZB[p], first, last, fp, fn);
+                            if constexpr (GRAD) {
+                                V dp = shfl_up_v(DT[p][W - 1], 32), dn = shfl_dn_v(DB[p][0], 32);
+                                if (from_x_prev) dp = xprev[XV + KP + p];
+                                if (from_x_next) dn = xnext[KP + p];
+                                shift_up_with<W>(DT[p], DB[p], first, last, dp, dn);
+                            }
+                        } else {
+                            V fn = shfl_dn_v(ZT[p][0], 32), fp = shfl_up_v(ZB[p][W - 1], 32);
+                            if (from_x_next) fn = xnext[p];
+                            if (from_x_prev) fp = xprev[XV + p];
+                            shift_down_with<W>(ZT[p], ZB[p], first, last, fn, fp);
+                        }
+                    }
+                }
+                if constexpr (su == SPS - 1) {
+                    // release the stage buffer; the LAST warp to release it refills it with the
+                    // stage NSTAGE ahead (no warp ever waits to act as the producer)
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int b = gst % NSTAGE;
+                        __threadfence_block();  // this warp's reads of buffer b happen-before the release
+                        if (atomicAdd(&released[b], 1u) == kNW - 1) {
+                            __threadfence_block();
+                            released[b] = 0;
+                            const int nxt = gst + NSTAGE;
+                            if (nxt < total_stages) {
+                                fence_proxy_async_smem();
+                                mbar_expect_tx(&full[b], G::STAGEB);
+                                bulk_g2s(stagebuf + (size_t)b * G::STAGEB, stage_src(nxt), G::STAGEB, &full[b]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    gst++;
+                }
+            });
+        }
+
+        // ---------------- store from the end layout (s_{R-1} forward, s_0 backward)
+        if (MODE == M_BWD && a.Y == nullptr) continue;
+#pragma unroll
+        for (int q = 0; q < W; q++) {
+            const int k = t * W + q;
+            const int pt = k, pb = ne - 1 - k;
+            int rt, rb;
+            if (UP) { rt = row_s0(pt); rb = row_s0(pb); }
+            else    { rt = row_sRm1(pt, ne); rb = row_sRm1(pb, ne); }
+            V vt[KP], vb[KP];
+#pragma unroll
+            for (int p = 0; p < KP; p++) {
+                if constexpr (GRAD) { vt[p] = DT[p][q]; vb[p] = DB[p][q]; }
+                else { vt[p] = ZT[p][q]; vb[p] = ZB[p][q]; }
+            }
+            if (!UP) {
+                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+#pragma unroll
+                for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
+            }
+            if (rt < n) IO::store(a.Y + (int64_t)rt * a.ldy, col0, a.m, a.vec_ok, vt);
+            if (rb < n) IO::store(a.Y + (int64_t)rb * a.ldy, col0, a.m, a.vec_ok, vb);
+        }
+    }
+    if constexpr (GRAD) {
+        if (grp >= 1) reduce_group(grp - 1);  // both halves: the last group is still pending
+        if (lane == 0) bulk_wait_all();
+    }
+}
+
+
+}  // namespace gk

@@ -116,6 +116,40 @@ __device__ __forceinline__ void shift_down(V (&T)[W], V (&B)[W], bool first, boo
     }
 }
 
+
+// The same two shifts with the cross-lane values supplied by the caller, for column groups that
+// span several warps (the values crossing a warp boundary come through shared memory).
+// forward direction: from_next = lane t+1's T[0], from_prev = lane t-1's B[W-1]
+template <int W, typename V>
+__device__ __forceinline__ void shift_down_with(V (&T)[W], V (&B)[W], bool first, bool last, V from_next,
+                                                V from_prev) {
+    V t_last = sel_v(last, B[W - 1], from_next);
+    V b_first = sel_v(first, T[1], from_prev);
+    V t0 = T[0];
+#pragma unroll
+    for (int q = 0; q < W - 1; q++) T[q] = T[q + 1];
+    T[W - 1] = t_last;
+    T[0] = sel_v(first, t0, T[0]);
+#pragma unroll
+    for (int q = W - 1; q >= 1; q--) B[q] = B[q - 1];
+    B[0] = b_first;
+}
+// backward direction: from_prev = lane t-1's T[W-1], from_next = lane t+1's B[0]
+template <int W, typename V>
+__device__ __forceinline__ void shift_up_with(V (&T)[W], V (&B)[W], bool first, bool last, V from_prev,
+                                              V from_next) {
+    V b_last = sel_v(last, T[W - 1], from_next);
+    V b0 = B[0];
+    V t0 = T[0];
+#pragma unroll
+    for (int q = W - 1; q >= 1; q--) T[q] = T[q - 1];
+    T[0] = sel_v(first, t0, from_prev);
+    T[1] = sel_v(first, b0, T[1]);
+#pragma unroll
+    for (int q = 0; q < W - 1; q++) B[q] = B[q + 1];
+    B[W - 1] = b_last;
+}
+
 // Row held at position p of s_0 (identity) and of s_{R-1} = (0, 2, 3, ..., n_eff-1, 1).
 __device__ __forceinline__ int row_s0(int p) { return p; }
 __device__ __forceinline__ int row_sRm1(int p, int ne) { return p == 0 ? 0 : (p == ne - 1 ? 1 : p + 1); }

@@ -1,0 +1,36 @@
+// ring_inst.cu -- one (W, L) configuration of the register-ring kernel, all four modes.
+// Compiled once per configuration with -DRING_W=.. -DRING_L=.. (parallel build, see build.py);
+// exports gk::ring_launch_<W>_<L>(mode, args, grid, stream).
+#include "common.cuh"
+
+#ifndef RING_W
+#error "RING_W / RING_L must be defined"
+#endif
+
+#define GK_CAT2(a, b, c) a##b##_##c
+#define GK_CAT(a, b, c) GK_CAT2(a, b, c)
+
+namespace gk {
+
+template <int W, int L, int MODE>
+static cudaError_t launch_wlm(const RingArgs &ra, int64_t grid, cudaStream_t st) {
+    constexpr size_t smem = RingGeom<W, L, MODE>::SMEM;
+    static_assert(smem <= 227 * 1024, "shared memory budget");
+    auto kfn = k_ring<W, L, MODE>;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kfn<<<(unsigned)grid, kThreads, smem, st>>>(ra);
+    return cudaGetLastError();
+}
+
+cudaError_t GK_CAT(ring_launch_, RING_W, RING_L)(int mode, const RingArgs &ra, int64_t grid, cudaStream_t st) {
+    switch (mode) {
+        case M_FWD: return launch_wlm<RING_W, RING_L, M_FWD>(ra, grid, st);
+        case M_BUILDU: return launch_wlm<RING_W, RING_L, M_BUILDU>(ra, grid, st);
+        case M_TRANS: return launch_wlm<RING_W, RING_L, M_TRANS>(ra, grid, st);
+        case M_BWD: return launch_wlm<RING_W, RING_L, M_BWD>(ra, grid, st);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace gk
