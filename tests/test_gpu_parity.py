@@ -72,7 +72,7 @@ def test_apply_parity(g, n, m):
     assert rel(Yt, Yto) <= TOL_Y
 
 
-@pytest.mark.parametrize("n", [2, 3, 6, 8, 16, 33, 64, 256, 1024, 2047])
+@pytest.mark.parametrize("n", [2, 3, 6, 8, 16, 33, 64, 256, 1024, 2047, 4096])
 def test_build_U_parity(g, n):
     th = synth.theta(n * (n - 1) // 2, seed=5)
     U = g.build_U(_cuda(th), n).cpu().numpy()
@@ -210,6 +210,46 @@ def test_full_size_sampled(g, n, m):
     d1, _ = g.backward(tt, Y[:, :h].contiguous(), dYt[:, :h].contiguous(), want_dX=False)
     d2, _ = g.backward(tt, Y[:, h:].contiguous(), dYt[:, h:].contiguous(), want_dX=False)
     assert rel((d1 + d2).cpu().numpy(), dth.cpu().numpy()) <= 1e-5
+
+
+@pytest.mark.parametrize("n,m", [(4096, 20), (4095, 9)])
+def test_multiwarp_ring_parity(g, n, m):
+    """C4 sizes: column groups spanning four warps (L = 128 lanes)."""
+    th, X, dY, _ = _inputs(n, m, seed=n)
+    tt, Xt, dYt = _cuda(th), _cuda(X), _cuda(dY)
+    Y = g.apply(tt, Xt)
+    dth, dX = g.backward(tt, Y, dYt)
+    Yo = oracle.apply(n, th, X.astype(np.float64))
+    dto, dXo = oracle.backward(n, th, X.astype(np.float64), dY.astype(np.float64))
+    assert rel(Y.cpu().numpy(), Yo) <= TOL_Y
+    assert rel(dth.cpu().numpy(), dto) <= TOL_DTH
+    assert rel(dX.cpu().numpy(), dXo) <= TOL_Y
+    Yt = g.apply(tt, Xt, transpose=True).cpu().numpy()
+    assert rel(Yt, oracle.apply(n, th, X.astype(np.float64), transpose=True)) <= TOL_Y
+
+
+def test_c4_ubuild_gradient_full(g):
+    """C4 (n=4096): U from all 8.4M angles + the gradient w.r.t. all of them, in the bench
+    configuration; U on sampled columns vs the oracle, U^T U = I on a row sample, dtheta of block
+    b_1 vs its closed form (Y dY^T - dY Y^T)_{ij} with Y = U, dY = Gamma."""
+    n = 4096
+    th = synth.theta(n * (n - 1) // 2, seed=4)
+    Gm = synth.normal_matrix(n, n, seed=4, tid=synth.TID_GAMMA)
+    tt = _cuda(th)
+    U = g.build_U(tt, n)
+    Gt = _cuda(Gm)
+    dth, _ = g.backward(tt, U, Gt, want_dX=False)
+    cols = np.array([0, 1, 777, 2048, 4095])
+    E = np.zeros((n, cols.size))
+    E[cols, np.arange(cols.size)] = 1.0
+    Uo_cols = oracle.apply(n, th, E)
+    assert np.abs(U.cpu().numpy()[:, cols] - Uo_cols).max() <= 1e-5 * np.sqrt(n)
+    Ud = U.double()
+    rows = torch.tensor([0, 5, 1000, 4095], device="cuda")
+    orth = (Ud[rows] @ Ud.T - torch.eye(n, device="cuda", dtype=torch.float64)[rows]).abs().max().item()
+    assert orth <= 1e-4
+    f, want = _closed_form_block_dtheta(g, n, U, Gt, 0)
+    assert rel(dth.cpu().numpy()[f], want) <= TOL_DTH
 
 
 def test_c5_odd_masked_subset(g):
