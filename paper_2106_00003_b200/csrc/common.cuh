@@ -42,8 +42,12 @@ __host__ __device__ inline int pos_of(int i, int r, int ne) {
     return 1 + ((i - 1 + r) % R);
 }
 
-constexpr int kNW = 8;           // warps per CTA of the ring kernel
-constexpr int kThreads = kNW * 32;
+constexpr int kNW = 8;           // warps per CTA of the backward ring kernel
+#ifndef GK_FWD_WARPS
+#define GK_FWD_WARPS 8
+#endif
+constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose ring kernels
+__host__ __device__ constexpr int ring_warps(int mode) { return mode == 3 ? kNW : kNWF; }
 
 enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3 };
 
@@ -229,6 +233,18 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// dtheta-partial geometry of the backward ring (shared by the kernel, the host's workspace sizing
+// and the stage-2 reduction): RG steps per reduction group, NSUM warps per chunk, OUTCH chunks
+// reduced per warp; per CTA the partial holds, for every group, NW blocks of RG x OUTCH float4.
+struct RedGeom {
+    int LW, H, NCHW, NSUM, OUTCH, RG, NW;
+};
+__host__ __device__ constexpr RedGeom red_geom(int W, int L) {
+    int LW = L < 32 ? L : 32, H = L / LW, NCHW = (W / 4) * LW, NSUM = kNW / H;
+    int RG = (NCHW >= 256 || (H > 1 && NCHW >= 128)) ? 2 : 4;
+    return RedGeom{LW, H, NCHW, NSUM, (NCHW + NSUM - 1) / NSUM, RG, kNW};
+}
+
 // Compile-time geometry of one ring configuration: W slots per lane, L lanes per column group
 // (L < 32: several groups per warp; L = 32 H: a group spans H warps).
 template <int W, int L, int MODE>
@@ -238,14 +254,15 @@ struct RingGeom {
     static constexpr int LW = L < 32 ? L : 32;      // lanes of a group inside one warp
     static constexpr int H = L / LW;                // warps per column group
     static constexpr int LC = 32 / LW;              // column groups per warp
-    static constexpr int NGRP = kNW * LC / H;       // column groups per CTA
+    static constexpr int NW = ring_warps(MODE);      // warps per CTA
+    static constexpr int NGRP = NW * LC / H;        // column groups per CTA
     static constexpr int K = kcols(W, MODE);        // columns per thread
     static constexpr bool GRAD = (MODE == M_BWD);
     static constexpr int KP = (K + 1) / 2;          // packed register pairs per slot
     // table rows per TMA stage: a power of two dividing W/2 with a stage of at most 16 KB
-    static constexpr int sps_pick() {
+    static constexpr int sps_pick() {  // stages of <= 32 KB forward, <= 16 KB next to the dtheta ring
         int v = W / 2;
-        while (v > 1 && v * S * 8 > 16384) v /= 2;
+        while (v > 1 && v * S * 8 > ((MODE == M_BWD) ? 16384 : 32768)) v /= 2;
         return v;
     }
     static constexpr int SPS = sps_pick();
@@ -255,19 +272,19 @@ struct RingGeom {
     static constexpr int NSTAGE_ = (GRAD ? 65536 : 98304) / STAGEB;
     static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
     // backward dtheta sums: per-warp ring of NG groups of RG steps, reduced one group later
-    static constexpr int RG = ((W / 4) * LW >= 256 || (H > 1 && (W / 4) * LW >= 128)) ? 2 : 4;  // steps per group
+    static constexpr int RG = red_geom(W, L).RG;     // steps per reduction group
     static constexpr int NG = 2;                    // groups in flight
     static constexpr int D = RG * NG;               // ring depth in steps
     static constexpr int NCH = S / 4;               // float4 chunks of a step's per-slot sums
     static constexpr int NCHW = (W / 4) * LW;       // chunks held by one warp (= NCH / H)
-    static constexpr int NSUM = kNW / H;            // warps contributing to each chunk
+    static constexpr int NSUM = NW / H;             // warps contributing to each chunk
     static constexpr int OUTCH = (NCHW + NSUM - 1) / NSUM;  // chunks reduced per warp (max)
     static constexpr int XV = GRAD ? 2 * KP : KP;   // packed values crossing a warp boundary per direction
     static constexpr size_t OFF_STAGE = 256;
     static constexpr size_t OFF_X = OFF_STAGE + (size_t)NSTAGE * STAGEB;
-    static constexpr size_t OFF_RED = OFF_X + (H > 1 ? (size_t)2 * kNW * 2 * XV * 8 : 0);
-    static constexpr size_t OFF_OUT = OFF_RED + (GRAD ? (size_t)kNW * D * NCHW * 16 : 0);
-    static constexpr size_t SMEM = OFF_OUT + (GRAD ? (size_t)kNW * NG * RG * OUTCH * 16 : 0);
+    static constexpr size_t OFF_RED = OFF_X + (H > 1 ? (size_t)2 * NW * 2 * XV * 8 : 0);
+    static constexpr size_t OFF_OUT = OFF_RED + (GRAD ? (size_t)NW * D * NCHW * 16 : 0);
+    static constexpr size_t SMEM = OFF_OUT + (GRAD ? (size_t)NW * NG * RG * OUTCH * 16 : 0);
 };
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -283,7 +300,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // a chunk range) and leave the SM as TMA bulk reduce-adds into this CTA's private partial rows
 // (fixed order, no atomics => deterministic).
 template <int W, int L, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
+__global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const RingArgs a) {
     using G = RingGeom<W, L, MODE>;
     using IO = ColIO<G::K>;
     using V = typename IO::V;
@@ -293,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                   NSTAGE = G::NSTAGE;
     constexpr int RG = G::RG, NG = G::NG, D = G::D, NCHW = G::NCHW, NSUM = G::NSUM, OUTCH = G::OUTCH;
     constexpr int XV = G::XV;
+    constexpr int NW = G::NW;
     constexpr bool UP = (MODE == M_TRANS || MODE == M_BWD);  // walk b_1 -> b_R (inverse rotations)
     constexpr bool GRAD = G::GRAD;
     static_assert(W % SPS == 0 && W % RG == 0 && W % 4 == 0 && W % 2 == 0, "geometry");
@@ -304,9 +322,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
     uint64_t *rfull = full + NSTAGE + (NSTAGE + 1) / 2;
     uint64_t *rempty = rfull + NG;
     uint8_t *stagebuf = smem + G::OFF_STAGE;
-    V *xbuf = reinterpret_cast<V *>(smem + G::OFF_X);                 // [2][kNW][2][XV]
-    float4 *red = reinterpret_cast<float4 *>(smem + G::OFF_RED);   // [kNW][D][NCHW]
-    float4 *outb = reinterpret_cast<float4 *>(smem + G::OFF_OUT);  // [kNW][NG][RG][OUTCH]
+    V *xbuf = reinterpret_cast<V *>(smem + G::OFF_X);                 // [2][NW][2][XV]
+    float4 *red = reinterpret_cast<float4 *>(smem + G::OFF_RED);   // [NW][D][NCHW]
+    float4 *outb = reinterpret_cast<float4 *>(smem + G::OFF_OUT);  // [NW][NG][RG][OUTCH]
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int h = warp % H;                       // which warp of its column group
@@ -328,8 +346,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
             released[i] = 0;
         }
         for (int i = 0; i < NG; i++) {
-            mbar_init(&rfull[i], kNW);
-            mbar_init(&rempty[i], kNW);
+            mbar_init(&rfull[i], NW);
+            mbar_init(&rempty[i], NW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async_smem();
@@ -392,14 +410,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
             mbar_arrive(&rempty[bi]);
             if (nch > 0) {
                 fence_proxy_async_smem();
+                // one bulk op per warp and group: this warp's RG x OUTCH block of the group
                 const int gs0 = gg * RG;
                 const int rho0 = gs0 % STEPS;
-                float *dst = a.partial + ((int64_t)blockIdx.x * STEPS + rho0) * S + (h * NCHW + ch0) * 4;
-#pragma unroll
-                for (int r = 0; r < RG; r++) {
-                    if (gs0 < STEPS) bulk_s2g_store(dst + (size_t)r * S, ob + r * OUTCH, (uint32_t)nch * 16);
-                    else bulk_s2g_reduce_add(dst + (size_t)r * S, ob + r * OUTCH, (uint32_t)nch * 16);
-                }
+                float *dst = a.partial + (((int64_t)blockIdx.x * (STEPS / RG) + rho0 / RG) * NW + warp) * (RG * OUTCH * 4);
+                if (gs0 < STEPS) bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
+                else bulk_s2g_reduce_add(dst, ob, (uint32_t)(RG * OUTCH * 16));
                 bulk_commit();
                 // successive slabs add into the same partial rows: keep them ordered
                 if (rho0 + RG == STEPS) bulk_wait_all();
@@ -492,16 +508,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                         if constexpr (GRAD) {
                             // dtheta contribution before this block's inverse rotation:
                             // dz_bottom * z_top - dz_top * z_bottom (Q_e structure)
-                            float c = 0.f;
+                            float c = cross_acc(0.f, DB[0][q], ZT[0][q], DT[0][q], ZB[0][q]);
 #pragma unroll
-                            for (int p = 0; p < KP; p++) c = cross_acc(c, DB[p][q], ZT[p][q], DT[p][q], ZB[p][q]);
+                            for (int p = 1; p < KP; p++) c = cross_acc(c, DB[p][q], ZT[p][q], DT[p][q], ZB[p][q]);
                             acc[LC > 1 ? q : (q & 3)] = c;
                         }
 #pragma unroll
                         for (int p = 0; p < KP; p++) {
                             if (UP) {
-                                rot_inv(ZT[p][q], ZB[p][q], tq, sq);
-                                if constexpr (GRAD) rot_inv(DT[p][q], DB[p][q], tq, sq);
+                                if constexpr (GRAD) rot_inv2(ZT[p][q], ZB[p][q], DT[p][q], DB[p][q], tq, sq);
+                                else rot_inv(ZT[p][q], ZB[p][q], tq, sq);
                             } else {
                                 rot_fwd(ZT[p][q], ZB[p][q], tq, sq);
                             }
@@ -552,7 +568,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                 } else {
                     // values crossing a warp boundary: publish, named barrier of the group, read
                     constexpr int par = uu & 1;  // double buffer (W is even)
-                    V *xo = xbuf + ((size_t)(par * kNW + warp) * 2) * XV;  // [0]: to warp h-1, [1]: to warp h+1
+                    V *xo = xbuf + ((size_t)(par * NW + warp) * 2) * XV;  // [0]: to warp h-1, [1]: to warp h+1
                     if (UP) {
                         // lane t+1 needs my T[W-1] (from_prev), lane t-1 needs my B[0] (from_next)
                         if (lane == 31) {
@@ -581,8 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                         }
                     }
                     named_bar(1 + cw, 32 * H);
-                    const V *xprev = xbuf + ((size_t)(par * kNW + warp - 1) * 2) * XV;  // warp h-1 of my group
-                    const V *xnext = xbuf + ((size_t)(par * kNW + warp + 1) * 2) * XV;  // warp h+1
+                    const V *xprev = xbuf + ((size_t)(par * NW + warp - 1) * 2) * XV;  // warp h-1 of my group
+                    const V *xnext = xbuf + ((size_t)(par * NW + warp + 1) * 2) * XV;  // warp h+1
                     const bool from_x_prev = (lane == 0 && h > 0), from_x_next = (lane == 31 && h < H - 1);
 #pragma unroll
                     for (int p = 0; p < KP; p++) {
@@ -612,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_ring(const RingArgs a) {
                     if (lane == 0) {
                         const int b = gst % NSTAGE;
                         __threadfence_block();  // this warp's reads of buffer b happen-before the release
-                        if (atomicAdd(&released[b], 1u) == kNW - 1) {
+                        if (atomicAdd(&released[b], 1u) == NW - 1) {
                             __threadfence_block();
                             released[b] = 0;
                             const int nxt = gst + NSTAGE;

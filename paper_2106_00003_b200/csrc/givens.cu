@@ -113,7 +113,7 @@ int dev_sms() {
 int64_t cols_per_slab(const Cfg &c, int mode) {
     if (!c.fast) return 32;
     int LW = c.L < 32 ? c.L : 32, H = c.L / LW, LC = 32 / LW;
-    return (int64_t)kNW * LC / H * kcols(c.W, mode);
+    return (int64_t)ring_warps(mode) * LC / H * kcols(c.W, mode);
 }
 
 int64_t grid_for(const Cfg &c, int mode, int64_t m) {
@@ -140,7 +140,12 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     L.partial = off;
     if (op == GIVENS_OP_BACKWARD) {
         int64_t g = grid_for(c, M_BWD, m);
-        off = al256(off + (size_t)g * 2 * c.S * c.S * 4);
+        size_t per_step = (size_t)c.S * 4;  // generic kernel: natural order
+        if (c.fast) {
+            const RedGeom rg = red_geom(c.W, c.L);
+            per_step = (size_t)rg.NW * rg.OUTCH * 16;  // >= S floats (padded when chunks don't split evenly)
+        }
+        off = al256(off + (size_t)g * 2 * c.S * per_step);
     }
     L.scratch = off;
     if (!c.fast) {
@@ -230,7 +235,7 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
 // ------------------------------------------------------------------ stage-2 dtheta reduction
 // dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in fixed CTA order (PAPER.md:768-781
 // "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0.
-__global__ void k_dtheta_reduce(int S, int W, int L, int G, const float *__restrict__ partial,
+__global__ void k_dtheta_reduce(int S, int W, int L, int G, int ring, const float *__restrict__ partial,
                                 const int32_t *__restrict__ amap, float *__restrict__ dtheta) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int rows = 2 * S;
@@ -243,17 +248,28 @@ __global__ void k_dtheta_reduce(int S, int W, int L, int G, const float *__restr
         return;
     }
     int rho = (int)(idx / S), k = (int)(idx % S);
-    // partial rows are stored in the ring kernel's chunk order: the warp slice h of lane t holds
-    // chunks h*NCHW + (q/4)*LW + (t % LW) covering slots t*W + 4*(q/4) + 0..3 (natural order
-    // when L = 1, W = S)
-    int LW = L < 32 ? L : 32;
-    int t = k / W, q = k % W, hs = t / LW, tl = t % LW;
-    int pos = ((hs * (W / 4) * LW + (q >> 2) * LW + tl) << 2) + (q & 3);
-    if (W % 4) pos = k;  // generic path (W = S, any S): natural order
+    int64_t pos, stride;
+    if (ring) {
+        // ring kernel layout: per CTA, per group of RG steps, NW warp blocks of RG x OUTCH float4;
+        // slot k (lane t = k / W of the group, slot q = k % W) is chunk ci = (q/4)*LW + t%LW of the
+        // warp slice t/LW, reduced by the warp c*H + slice that owns ci
+        const RedGeom rg = red_geom(W, L);
+        int t = k / W, q = k % W, hs = t / rg.LW, tl = t % rg.LW;
+        int ci = (q >> 2) * rg.LW + tl;
+        int c = 0;
+        while (c + 1 < rg.NSUM && ((c + 1) * rg.NCHW) / rg.NSUM <= ci) c++;
+        int j = ci - (c * rg.NCHW) / rg.NSUM;
+        int w = c * rg.H + hs;
+        int64_t blk = ((int64_t)(rho / rg.RG) * rg.NW + w) * rg.RG * rg.OUTCH;
+        pos = (blk + (rho % rg.RG) * rg.OUTCH + j) * 4 + (q & 3);
+        stride = (int64_t)rows * rg.NW * rg.OUTCH * 4;
+    } else {
+        pos = (int64_t)rho * S + k;  // generic kernel: natural order
+        stride = (int64_t)rows * S;
+    }
     float s = 0.f;
-    const float *p = partial + (int64_t)rho * S + pos;
-    int64_t stride = (int64_t)rows * S;
-    for (int c = 0; c < G; c++) s += p[(int64_t)c * stride];
+    const float *p = partial + pos;
+    for (int cc = 0; cc < G; cc++) s += p[(int64_t)cc * stride];
     dtheta[f] = (code & (1 << 30)) ? -s : s;
 }
 
@@ -629,7 +645,7 @@ int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     int64_t G = grid_for(c, M_BWD, m);
     int64_t tot = (int64_t)2 * c.S * c.S;
     k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
+        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, c.fast, reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
         dtheta);
     CUDA_TRY(cudaGetLastError());
     return 0;

@@ -36,10 +36,9 @@ __device__ __forceinline__ float cross_acc(float acc, float db, float zt, float 
     return fmaf(-dt, zb, fmaf(db, zt, acc));
 }
 __device__ __forceinline__ float cross_acc(float acc, float2 db, float2 zt, float2 dt, float2 zb) {
-    acc = fmaf(db.x, zt.x, acc);
-    acc = fmaf(db.y, zt.y, acc);
-    acc = fmaf(-dt.x, zb.x, acc);
-    return fmaf(-dt.y, zb.y, acc);
+    // packed: FMUL2 + FFMA2 + one FADD (scalar FFMAs with three distinct registers issue at half rate)
+    float2 s2 = __ffma2_rn(neg_v(dt), zb, __fmul2_rn(db, zt));
+    return acc + (s2.x + s2.y);
 }
 
 __device__ __forceinline__ float shfl_up_v(float v, int w) { return __shfl_up_sync(0xffffffffu, v, 1, w); }
@@ -71,6 +70,18 @@ __device__ __forceinline__ void rot_inv(V &x, V &y, float tq, float sq) {
     x = fma_v(tq, y, x);
     y = fma_v(-sq, x, y);
     x = fma_v(tq, y, x);
+}
+// The backward rotates Z and D by the same coefficients: issue their shears pairwise so the
+// second FFMA2 of each pair re-reads the coefficient from the operand reuse cache (an FFMA2 with
+// two register pairs and a fresh scalar reads three registers from one bank).
+template <typename V>
+__device__ __forceinline__ void rot_inv2(V &x, V &y, V &u, V &v, float tq, float sq) {
+    x = fma_v(tq, y, x);
+    u = fma_v(tq, v, u);
+    y = fma_v(-sq, x, y);
+    v = fma_v(-sq, u, v);
+    x = fma_v(tq, y, x);
+    u = fma_v(tq, v, u);
 }
 
 // ---- the ring shift ------------------------------------------------------------------------

@@ -19,7 +19,7 @@ static cudaError_t launch_wlm(const RingArgs &ra, int64_t grid, cudaStream_t st)
     auto kfn = k_ring<W, L, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kfn<<<(unsigned)grid, kThreads, smem, st>>>(ra);
+    kfn<<<(unsigned)grid, RingGeom<W, L, MODE>::NW * 32, smem, st>>>(ra);
     return cudaGetLastError();
 }
 
