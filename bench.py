@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-cols-per-step", type=int, default=128)
+    ap.add_argument("--no-ubuild", action="store_true", help="skip the U-build ms vs n table")
     return ap.parse_args()
 
 
@@ -164,14 +165,42 @@ def cpu_baseline(args, target_s: float = 12.0):
         oracle.backward(n, th, X, dY)
         return time.perf_counter() - t0
 
-    probe = 128
-    tp = run(probe)
-    cols = int(min(args.m, max(probe, probe * target_s / max(tp, 1e-3))))
-    cols = max(probe, cols // 64 * 64)
-    t = run(cols)
+    cols, t = 128, run(128)
+    while t < 0.5 * target_s and cols < args.m:  # grow the sample until it is ~target_s of CPU work
+        cols = int(min(args.m, max(2 * cols, cols * target_s / max(t, 1e-3)))) // 64 * 64
+        t = run(cols)
     return {"value": N * cols / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"first {cols} of {args.m} columns (n={n}): fp64 Alg. 1 forward + taped backward, "
                       f"{t:.1f} s wall"}
+
+
+def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 2048, 4096)):
+    """Device ms of build_U (forward from U <- I, Alg. 2) and of its gradient (Alg. 3 via the replay
+    backward with Gamma = dL/dU) per n; mean of 5 after warm-up (the paper used 50 runs)."""
+    table = {}
+    for n in ns:
+        N = n * (n - 1) // 2
+        th = torch.from_numpy(synth.theta(N, seed=SEED)).to(dev)
+        G = torch.from_numpy(synth.normal_matrix(n, n, SEED, synth.TID_GAMMA)).to(dev)
+        ws = g.workspace(g.OP_BACKWARD, n, n, dev)
+        U = torch.empty(n, n, device=dev)
+        dth = torch.empty(N, device=dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        g.build_U(th, n, out=U, ws=ws)
+        g.backward(th, U, G, ws=ws, recompute=False, dtheta=dth, want_dX=False)
+        tf = tb = 0.0
+        reps = 5
+        for _ in range(reps):
+            ev[0].record()
+            g.build_U(th, n, out=U, ws=ws)
+            ev[1].record()
+            g.backward(th, U, G, ws=ws, recompute=False, dtheta=dth, want_dX=False)
+            ev[2].record()
+            torch.cuda.synchronize()
+            tf += ev[0].elapsed_time(ev[1])
+            tb += ev[1].elapsed_time(ev[2])
+        table[str(n)] = {"build_U_ms": round(tf / reps, 4), "grad_ms": round(tb / reps, 4)}
+    return table
 
 
 # ------------------------------------------------------------------ our arm
@@ -294,6 +323,11 @@ def main():
         e2e = {"value": units / (float(te[0]) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 4 * n * m,
                "d2h_bytes_per_step": 4 * N, "ms_per_step": float(te[0])}
 
+    # ---------------- U-build ms vs n (the metric's second half; the paper's Fig. 2 axes)
+    ubuild = None
+    if rank == 0 and world == 1 and not args.no_ubuild:
+        ubuild = ubuild_table(g, torch, synth, dev)
+
     if rank == 0:
         sm_mhz = (clk or {}).get("sm_mhz")
         peak_clock = 1965.0
@@ -328,6 +362,8 @@ def main():
         }
         if e2e:
             out["e2e"] = e2e
+        if ubuild:
+            out["ubuild_ms_vs_n"] = ubuild
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out), flush=True)

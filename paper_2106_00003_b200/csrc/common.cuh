@@ -42,7 +42,10 @@ __host__ __device__ inline int pos_of(int i, int r, int ne) {
     return 1 + ((i - 1 + r) % R);
 }
 
-constexpr int kNW = 8;           // warps per CTA of the backward ring kernel
+#ifndef GK_BWD_WARPS
+#define GK_BWD_WARPS 8
+#endif
+constexpr int kNW = GK_BWD_WARPS;  // warps per CTA of the backward ring kernel
 #ifndef GK_FWD_WARPS
 #define GK_FWD_WARPS 8
 #endif
@@ -241,7 +244,7 @@ struct RedGeom {
 };
 __host__ __device__ constexpr RedGeom red_geom(int W, int L) {
     int LW = L < 32 ? L : 32, H = L / LW, NCHW = (W / 4) * LW, NSUM = kNW / H;
-    int RG = (NCHW >= 256 || (H > 1 && NCHW >= 128)) ? 2 : 4;
+    int RG = (NCHW >= 256 || (H > 1 && NCHW >= 128) || kNW > 8) ? 2 : 4;
     return RedGeom{LW, H, NCHW, NSUM, (NCHW + NSUM - 1) / NSUM, RG, kNW};
 }
 
@@ -547,11 +550,11 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                         if (lane == 0) mbar_arrive(&rfull[bi]);
                         // warps w and w+4 share an SMSP: the low half reduces the previous group
                         // here, the high half RG/2 steps earlier, so one of them keeps the FMA pipe busy
-                        if (warp < 4 && grp >= 1) reduce_group(grp - 1);
+                        if (((warp >> 2) & 1) == 0 && grp >= 1) reduce_group(grp - 1);
                         grp++;
                     }
                     if constexpr (r == RG / 2 - 1) {
-                        if (warp >= 4 && grp >= 1) reduce_group(grp - 1);
+                        if (((warp >> 2) & 1) == 1 && grp >= 1) reduce_group(grp - 1);
                     }
                 }
                 // ring shift to the next block's layout (Fig. 1)

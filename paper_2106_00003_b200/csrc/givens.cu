@@ -177,19 +177,37 @@ __global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uin
 
 // (2) per row: parity of flips among the blocks applied before block r in forward order
 // (forward applies b_R first), i.e. blocks r' > r. sig[r][row], sfin[row].
+// One warp per row: lane l owns a contiguous segment of blocks (highest blocks in lane 0); an
+// exclusive prefix XOR over the lanes gives each segment its starting parity.
 __global__ void k_sigma(int ne, const uint8_t *__restrict__ flip, uint8_t *__restrict__ sig,
                         uint8_t *__restrict__ sfin) {
-    int S = ne / 2, R = ne - 1;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int S = ne / 2, R = ne - 1;
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (i >= ne) return;
-    uint8_t par = 0;
-    for (int r = R - 1; r >= 0; r--) {
-        sig[(int64_t)r * ne + i] = par;
+    const int seg = (R + 31) / 32;
+    const int hi = R - 1 - lane * seg;          // first (highest) block of this lane's segment
+    const int lo = max(hi - seg + 1, 0);
+    auto flip_at = [&](int r) {
         int p = pos_of(i, r, ne);
         int k = p < ne - 1 - p ? p : ne - 1 - p;
-        par ^= flip[(int64_t)r * S + k];
+        return (uint32_t)flip[(int64_t)r * S + k];
+    };
+    uint32_t x = 0;
+    for (int r = hi; r >= lo; r--) x ^= flip_at(r);
+    // exclusive prefix XOR over lanes 0..lane-1
+    uint32_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl ^= v;
     }
-    sfin[i] = par;
+    uint32_t par = incl ^ x;
+    for (int r = hi; r >= lo; r--) {
+        sig[(int64_t)r * ne + i] = (uint8_t)par;
+        par ^= flip_at(r);
+    }
+    if (lane == 31) sfin[i] = (uint8_t)incl;
 }
 
 __device__ __forceinline__ int coef_pos(int k, int W, int L) {
@@ -482,7 +500,7 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
     int64_t RS = (int64_t)c.R * c.S;
     k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, ws + L.flip);
     CUDA_TRY(cudaGetLastError());
-    k_sigma<<<(unsigned)((c.ne + 127) / 128), 128, 0, st>>>(c.ne, ws + L.flip, ws + L.sig, ws + L.sfin);
+    k_sigma<<<(unsigned)((c.ne + 7) / 8), 256, 0, st>>>(c.ne, ws + L.flip, ws + L.sig, ws + L.sfin);
     CUDA_TRY(cudaGetLastError());
     int64_t tot = (int64_t)(c.R + 2) * c.S;
     int W = c.fast ? c.W : c.S, Lq = c.fast ? c.L : 1;
