@@ -176,3 +176,56 @@ def givens_apply(theta, X, mask=None):
 
 def version() -> str:
     return lib().givens_version().decode()
+
+
+class HostPipeline:
+    """Training-style loop over host batches: the host->device copy of batch k+1 (on a copy
+    stream, from pinned memory) overlaps the forward + backward of batch k (on the compute stream);
+    dtheta of every batch is copied back to pinned host memory.
+
+        pipe = HostPipeline(theta, n, m)
+        pipe.submit(X0, dY0)
+        for k in range(K):
+            if k + 1 < K: pipe.submit(X[k+1], dY[k+1])
+            dth_host = pipe.step()          # forward + backward of the oldest submitted batch
+    """
+
+    def __init__(self, theta, n, m, mask=None, want_dX=False, device=None, allreduce=None):
+        dev = device or theta.device
+        self.theta, self.mask, self.n, self.m, self.want_dX = theta, mask, n, m, want_dX
+        self.allreduce = allreduce
+        self.compute = torch.cuda.current_stream(dev)
+        self.copy = torch.cuda.Stream(dev)
+        self.X = [torch.empty(n, m, device=dev) for _ in range(2)]
+        self.dY = [torch.empty(n, m, device=dev) for _ in range(2)]
+        self.Y = torch.empty(n, m, device=dev)
+        self.dX = torch.empty(n, m, device=dev) if want_dX else None
+        self.dth = torch.empty(num_angles(n), device=dev)
+        self.dth_host = torch.empty(num_angles(n), dtype=torch.float32).pin_memory()
+        self.ws = workspace(OP_BACKWARD, n, m, dev)
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        self.n_sub = 0
+        self.n_done = 0
+
+    def submit(self, X_host, dY_host):
+        s = self.n_sub % 2
+        with torch.cuda.stream(self.copy):
+            self.copy.wait_event(self.free[s])       # the compute that last read slot s is done
+            self.X[s].copy_(X_host, non_blocking=True)
+            self.dY[s].copy_(dY_host, non_blocking=True)
+            self.ready[s].record(self.copy)
+        self.n_sub += 1
+
+    def step(self):
+        s = self.n_done % 2
+        self.compute.wait_event(self.ready[s])
+        apply(self.theta, self.X[s], mask=self.mask, out=self.Y, ws=self.ws)
+        backward(self.theta, self.Y, self.dY[s], mask=self.mask, ws=self.ws, recompute=False,
+                 dtheta=self.dth, dX=self.dX, want_dX=self.want_dX)
+        self.free[s].record(self.compute)
+        if self.allreduce is not None:
+            self.allreduce(self.dth)
+        self.dth_host.copy_(self.dth, non_blocking=True)
+        self.n_done += 1
+        return self.dth_host
