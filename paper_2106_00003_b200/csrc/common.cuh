@@ -417,8 +417,16 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 const int gs0 = gg * RG;
                 const int rho0 = gs0 % STEPS;
                 float *dst = a.partial + (((int64_t)blockIdx.x * (STEPS / RG) + rho0 / RG) * NW + warp) * (RG * OUTCH * 4);
+                (void)dst;
+#if defined(GK_EXP_L2ONLY)
+                dst = a.partial + ((int64_t)(blockIdx.x & 7) * (STEPS / RG) * NW + warp) * (RG * OUTCH * 4);
+                bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
+#elif defined(GK_EXP_STOREONLY)
+                bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
+#else
                 if (gs0 < STEPS) bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
                 else bulk_s2g_reduce_add(dst, ob, (uint32_t)(RG * OUTCH * 16));
+#endif
                 bulk_commit();
                 // successive slabs add into the same partial rows: keep them ordered
                 if (rho0 + RG == STEPS) bulk_wait_all();
