@@ -174,9 +174,10 @@ def cpu_baseline(args, target_s: float = 12.0):
                       f"{t:.1f} s wall"}
 
 
-def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 2048, 4096)):
+def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 4096)):
     """Device ms of build_U (forward from U <- I, Alg. 2) and of its gradient (Alg. 3 via the replay
-    backward with Gamma = dL/dU) per n; mean of 5 after warm-up (the paper used 50 runs)."""
+    backward with Gamma = dL/dU) per n; mean of 5 after warm-up (the paper used 50 runs).
+    n = 1120 and 2000 are the paper's CPU and GPU maxima."""
     table = {}
     for n in ns:
         N = n * (n - 1) // 2

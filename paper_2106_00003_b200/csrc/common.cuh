@@ -107,6 +107,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // ------------------------------------------------------------------ the register-ring kernel
 struct RingArgs {
     int n, ne;
+    int La;           // active lanes per column group (== L except for idle-lane configurations)
     int64_t m;
     const float *X;   // FWD/TRANS: input; BWD: Y
     int64_t ldx;
@@ -309,8 +310,13 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     using V = typename IO::V;
     constexpr int KP = IO::KP;
     constexpr int K = G::K;
-    constexpr int S = G::S, STEPS = G::STEPS, LW = G::LW, H = G::H, LC = G::LC, SPS = G::SPS,
-                  NSTAGE = G::NSTAGE;
+    constexpr int LW = G::LW, H = G::H, LC = G::LC, SPS = G::SPS, NSTAGE = G::NSTAGE;
+    // active geometry: L lanes are instantiated, the last warp of a group may leave lanes idle
+    // (S = W * La with La in (L - 32, L]); buffers are sized for the instantiated maximum
+    const int La = (H == 1 && LC > 1) ? L : a.La;
+    const int S = W * La, STEPS = 2 * S;
+    const int rowb = S * 8;                       // bytes per table row
+    const uint32_t stage_bytes = (uint32_t)(SPS * rowb);
     constexpr int RG = G::RG, NG = G::NG, D = G::D, NCHW = G::NCHW, NSUM = G::NSUM, OUTCH = G::OUTCH;
     constexpr int XV = G::XV;
     constexpr int NW = G::NW;
@@ -335,7 +341,9 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     const int g = lane / LW;                      // column group inside the warp (LC > 1)
     const int tl = lane % LW;                     // lane inside the group's warp slice
     const int t = h * LW + tl;                    // lane inside the column group
-    const bool first = (t == 0), last = (t == L - 1);
+    const bool first = (t == 0), last = (t == La - 1);
+    const bool active = t < La;
+    const int tc = active ? t : La - 1;          // idle lanes read a valid coefficient slot
     const int ne = a.ne, n = a.n;
     const int64_t C = (int64_t)G::NGRP * K;
     const int my_slabs = (int)((a.nslabs - blockIdx.x + gridDim.x - 1) / gridDim.x);
@@ -367,12 +375,12 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     auto stage_src = [&](int gst) -> const uint8_t * {
         int j = gst % (STEPS / SPS);
         int rho0 = UP ? j * SPS : (STEPS - (j + 1) * SPS + 1);
-        return a.coef + (int64_t)rho0 * G::ROWB;
+        return a.coef + (int64_t)rho0 * rowb;
     };
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGE && s < total_stages; s++) {
-            mbar_expect_tx(&full[s], G::STAGEB);
-            bulk_g2s(stagebuf + (size_t)s * G::STAGEB, stage_src(s), G::STAGEB, &full[s]);
+            mbar_expect_tx(&full[s], stage_bytes);
+            bulk_g2s(stagebuf + (size_t)s * G::STAGEB, stage_src(s), stage_bytes, &full[s]);
         }
     }
 
@@ -417,16 +425,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 const int gs0 = gg * RG;
                 const int rho0 = gs0 % STEPS;
                 float *dst = a.partial + (((int64_t)blockIdx.x * (STEPS / RG) + rho0 / RG) * NW + warp) * (RG * OUTCH * 4);
-                (void)dst;
-#if defined(GK_EXP_L2ONLY)
-                dst = a.partial + ((int64_t)(blockIdx.x & 7) * (STEPS / RG) * NW + warp) * (RG * OUTCH * 4);
-                bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
-#elif defined(GK_EXP_STOREONLY)
-                bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
-#else
                 if (gs0 < STEPS) bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
                 else bulk_s2g_reduce_add(dst, ob, (uint32_t)(RG * OUTCH * 16));
-#endif
                 bulk_commit();
                 // successive slabs add into the same partial rows: keep them ordered
                 if (rho0 + RG == STEPS) bulk_wait_all();
@@ -450,6 +450,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             int rt, rb;
             if (UP) { rt = row_sRm1(pt, ne); rb = row_sRm1(pb, ne); }
             else    { rt = row_s0(pt);       rb = row_s0(pb); }
+            if (!active) rt = rb = n;  // idle lanes hold zeros and never store
             V vt[KP], vb[KP];
             if constexpr (MODE == M_BUILDU) {
 #pragma unroll
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     __syncwarp();
                 }
                 const float4 *row4 = reinterpret_cast<const float4 *>(
-                    stagebuf + (gst % NSTAGE) * G::STAGEB + (UP ? su : (SPS - 1 - su)) * G::ROWB);
+                    stagebuf + (gst % NSTAGE) * G::STAGEB + (UP ? su : (SPS - 1 - su)) * rowb);
                 constexpr int r = uu % RG;
                 int bi = 0;
                 float4 *ring_dst = nullptr;
@@ -511,7 +512,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 float acc[GRAD ? (LC > 1 ? W : 4) : 1];
 #pragma unroll
                 for (int pp = 0; pp < W / 2; pp++) {
-                    const float4 cf = row4[pp * L + t];
+                    const float4 cf = row4[pp * La + tc];
 #pragma unroll
                     for (int hh = 0; hh < 2; hh++) {
                         const int q = 2 * pp + hh;
@@ -645,8 +646,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                             const int nxt = gst + NSTAGE;
                             if (nxt < total_stages) {
                                 fence_proxy_async_smem();
-                                mbar_expect_tx(&full[b], G::STAGEB);
-                                bulk_g2s(stagebuf + (size_t)b * G::STAGEB, stage_src(nxt), G::STAGEB, &full[b]);
+                                mbar_expect_tx(&full[b], stage_bytes);
+                                bulk_g2s(stagebuf + (size_t)b * G::STAGEB, stage_src(nxt), stage_bytes, &full[b]);
                             }
                         }
                     }
@@ -665,6 +666,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             int rt, rb;
             if (UP) { rt = row_s0(pt); rb = row_s0(pb); }
             else    { rt = row_sRm1(pt, ne); rb = row_sRm1(pb, ne); }
+            if (!active) rt = rb = n;
             V vt[KP], vb[KP];
 #pragma unroll
             for (int p = 0; p < KP; p++) {

@@ -32,7 +32,7 @@
 namespace gk {
 #define GK_DECL(W, L) cudaError_t ring_launch_##W##_##L(int mode, const RingArgs &ra, int64_t grid, cudaStream_t st);
 GK_DECL(4, 1) GK_DECL(8, 1) GK_DECL(16, 1) GK_DECL(32, 1) GK_DECL(16, 4) GK_DECL(16, 8) GK_DECL(16, 16)
-GK_DECL(16, 32) GK_DECL(8, 64) GK_DECL(16, 64) GK_DECL(32, 32) GK_DECL(16, 128)
+GK_DECL(16, 32) GK_DECL(8, 64) GK_DECL(16, 64) GK_DECL(32, 32) GK_DECL(16, 128) GK_DECL(8, 32) GK_DECL(8, 128)
 #undef GK_DECL
 }  // namespace gk
 
@@ -61,7 +61,8 @@ int fail(int code, const char *fmt, ...) {
 
 // ------------------------------------------------------------------ configuration
 struct Cfg {
-    int ne, S, R, W, L, fast;  // fast: register ring kernel (else generic)
+    int ne, S, R, W, L, fast;  // fast: register ring kernel (else generic); L = instantiated lanes
+    int La;                    // active lanes per column group (S = W * La; La <= L)
     int rowbytes;              // bytes per table row (S float2, padded to 16)
 };
 
@@ -91,6 +92,18 @@ Cfg make_cfg(int n) {
         if (wpref == 32) { c.W = 32; c.L = 32; }
     } else if (c.S == 2048) {
         c.fast = 1; c.W = 16; c.L = 128;
+    }
+    c.La = c.L;
+    if (!c.fast) {
+        // any other S: the ring with idle lanes at the end of the last warp of each column group
+        // (S = W * La, La active lanes out of L = 32, 64 or 128 instantiated ones)
+        for (int w : {16, 8}) {
+            if (c.S % w == 0 && c.S / w >= 2 && c.S / w <= 128) {
+                c.fast = 1; c.W = w; c.La = c.S / w;
+                c.L = c.La <= 32 ? 32 : (c.La <= 64 ? 64 : 128);
+                break;
+            }
+        }
     }
     c.rowbytes = ((c.S * 8) + 15) / 16 * 16;  // == S*8 for every ring configuration
     return c;
@@ -378,15 +391,15 @@ __global__ void __launch_bounds__(32) k_generic(const GenArgs a) {
 
 // ------------------------------------------------------------------ index trace
 template <int W>
-__global__ void k_trace(int ne, int L, int up, int32_t *out) {
+__global__ void k_trace(int ne, int L, int width, int up, int32_t *out) {
     const int lane = threadIdx.x;
-    const int t = lane % L;          // every group runs (shuffles need the full warp)
-    const bool writer = lane < L;    // group 0 records
+    const int t = lane % width;      // every lane runs (shuffles need the full warp)
+    const bool writer = lane < L;    // group 0's active lanes record
     const bool first = t == 0, last = t == L - 1;
     const int S = ne / 2, R = ne - 1;
     float T[W], B[W];
     for (int q = 0; q < W; q++) {
-        int k = t * W + q;
+        int k = (t < L ? t : L - 1) * W + q;
         T[q] = (float)(up ? row_sRm1(k, ne) : row_s0(k));
         B[q] = (float)(up ? row_sRm1(ne - 1 - k, ne) : row_s0(ne - 1 - k));
     }
@@ -403,8 +416,8 @@ __global__ void k_trace(int ne, int L, int up, int32_t *out) {
                     out[((int64_t)r * S + k) * 2 + 1] = a < b ? b : a;
                 }
             }
-            if (up) shift_up<W>(T, B, first, last, L);
-            else shift_down<W>(T, B, first, last, L);
+            if (up) shift_up<W>(T, B, first, last, width);
+            else shift_down<W>(T, B, first, last, width);
         }
     }
 }
@@ -412,14 +425,14 @@ __global__ void k_trace(int ne, int L, int up, int32_t *out) {
 // the same for column groups spanning H = L/32 warps (one CTA of L threads): the values that
 // cross a warp boundary go through shared memory, as in k_ring
 template <int W>
-__global__ void k_trace_multi(int ne, int L, int up, int32_t *out) {
+__global__ void k_trace_multi(int ne, int La, int up, int32_t *out) {
     __shared__ float xs[2][32][2];  // [parity][warp][0: to warp h-1, 1: to warp h+1]
-    const int t = threadIdx.x, lane = t & 31, h = t >> 5, H = L / 32;
-    const bool first = t == 0, last = t == L - 1;
+    const int t = threadIdx.x, lane = t & 31, h = t >> 5, H = blockDim.x / 32;
+    const bool first = t == 0, last = t == La - 1;
     const int S = ne / 2, R = ne - 1;
     float T[W], B[W];
     for (int q = 0; q < W; q++) {
-        int k = t * W + q;
+        int k = (t < La ? t : La - 1) * W + q;
         T[q] = (float)(up ? row_sRm1(k, ne) : row_s0(k));
         B[q] = (float)(up ? row_sRm1(ne - 1 - k, ne) : row_s0(ne - 1 - k));
     }
@@ -427,7 +440,7 @@ __global__ void k_trace_multi(int ne, int L, int up, int32_t *out) {
 #pragma unroll
         for (int uu = 0; uu < W; uu++) {
             int u = body * W + uu, par = u & 1;
-            if (u >= 1) {
+            if (u >= 1 && t < La) {
                 int r = up ? (u - 1) : (R - u);
                 for (int q = 0; q < W; q++) {
                     int k = t * W + q;
@@ -478,7 +491,7 @@ using namespace gk;
 
 // ring configurations compiled in ring_inst.cu (one object per (W, L))
 #define GK_RING_CONFIGS(X) X(4, 1) X(8, 1) X(16, 1) X(32, 1) X(16, 4) X(16, 8) X(16, 16) X(16, 32) X(8, 64) \
-    X(16, 64) X(32, 32) X(16, 128)
+    X(16, 64) X(32, 32) X(16, 128) X(8, 32) X(8, 128)
 
 int launch_ring(int mode, const Cfg &c, RingArgs &ra, int64_t grid, cudaStream_t st) {
     cudaError_t e = cudaErrorInvalidConfiguration;
@@ -503,7 +516,7 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
     k_sigma<<<(unsigned)((c.ne + 7) / 8), 256, 0, st>>>(c.ne, ws + L.flip, ws + L.sig, ws + L.sfin);
     CUDA_TRY(cudaGetLastError());
     int64_t tot = (int64_t)(c.R + 2) * c.S;
-    int W = c.fast ? c.W : c.S, Lq = c.fast ? c.L : 1;
+    int W = c.fast ? c.W : c.S, Lq = c.fast ? c.La : 1;
     k_coef<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, c.rowbytes, theta, mask, ws + L.flip,
                                                           ws + L.sig, ws + L.coef,
                                                           reinterpret_cast<int32_t *>(ws + L.amap));
@@ -537,7 +550,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
     int64_t grid = grid_for(c, mode, m);
     if (c.fast) {
         RingArgs ra;
-        ra.n = n; ra.ne = c.ne;
+        ra.n = n; ra.ne = c.ne; ra.La = c.La;
         ra.m = m; ra.X = X; ra.ldx = ldx; ra.dY = dY; ra.lddy = lddy; ra.Y = Y; ra.ldy = ldy;
         ra.coef = ws + L.coef; ra.sfin = ws + L.sfin;
         ra.partial = reinterpret_cast<float *>(ws + L.partial);
@@ -676,16 +689,17 @@ int givens_index_trace(int32_t n, int direction, int32_t *out_dev, void *stream)
     int up = direction ? 1 : 0;
     if (c.fast && c.L > 32) {
         switch (c.W) {
-            case 8: k_trace_multi<8><<<1, c.L, 0, st>>>(c.ne, c.L, up, out_dev); break;
-            case 16: k_trace_multi<16><<<1, c.L, 0, st>>>(c.ne, c.L, up, out_dev); break;
-            case 32: k_trace_multi<32><<<1, c.L, 0, st>>>(c.ne, c.L, up, out_dev); break;
+            case 8: k_trace_multi<8><<<1, c.L, 0, st>>>(c.ne, c.La, up, out_dev); break;
+            case 16: k_trace_multi<16><<<1, c.L, 0, st>>>(c.ne, c.La, up, out_dev); break;
+            case 32: k_trace_multi<32><<<1, c.L, 0, st>>>(c.ne, c.La, up, out_dev); break;
         }
     } else if (c.fast) {
+        const int width = c.L < 32 ? c.L : 32;
         switch (c.W) {
-            case 4: k_trace<4><<<1, 32, 0, st>>>(c.ne, c.L, up, out_dev); break;
-            case 8: k_trace<8><<<1, 32, 0, st>>>(c.ne, c.L, up, out_dev); break;
-            case 16: k_trace<16><<<1, 32, 0, st>>>(c.ne, c.L, up, out_dev); break;
-            case 32: k_trace<32><<<1, 32, 0, st>>>(c.ne, c.L, up, out_dev); break;
+            case 4: k_trace<4><<<1, 32, 0, st>>>(c.ne, c.La, width, up, out_dev); break;
+            case 8: k_trace<8><<<1, 32, 0, st>>>(c.ne, c.La, width, up, out_dev); break;
+            case 16: k_trace<16><<<1, 32, 0, st>>>(c.ne, c.La, width, up, out_dev); break;
+            case 32: k_trace<32><<<1, 32, 0, st>>>(c.ne, c.La, width, up, out_dev); break;
         }
     } else {
         int64_t RS = (int64_t)c.R * c.S;

@@ -47,11 +47,13 @@ def _cuda(a):
     return None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-ALL_N = [2, 3, 4, 5, 6, 7, 8, 9, 12, 15, 16, 17, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 255, 256, 300,
-         511, 512, 1023, 1024, 2047, 2048]
+ALL_N = [2, 3, 4, 5, 6, 7, 8, 9, 12, 15, 16, 17, 31, 32, 33, 48, 63, 64, 65, 96, 100, 127, 128, 129, 160, 255,
+         256, 300, 511, 512, 768, 1023, 1024, 1120, 2047, 2048]
+# ring configurations with idle lanes (S = W * La, La not a power of two): 48, 96, 160, 768, 1120,
+# and below 1535, 2000 (W=8, La=125 of 128), 2400 (a fully idle trailing warp)
 
 
-@pytest.mark.parametrize("n", ALL_N + [4096])
+@pytest.mark.parametrize("n", ALL_N + [1535, 2000, 2400, 4096])
 @pytest.mark.parametrize("direction", [0, 1])
 def test_index_trace_bit_exact(g, n, direction):
     """The kernels' on-device data movement pairs exactly the schedule's rows (bit-exact)."""
@@ -212,7 +214,7 @@ def test_full_size_sampled(g, n, m):
     assert rel((d1 + d2).cpu().numpy(), dth.cpu().numpy()) <= 1e-5
 
 
-@pytest.mark.parametrize("n,m", [(4096, 20), (4095, 9)])
+@pytest.mark.parametrize("n,m", [(4096, 20), (4095, 9), (1535, 11), (2000, 10), (2400, 7)])
 def test_multiwarp_ring_parity(g, n, m):
     """C4 sizes: column groups spanning four warps (L = 128 lanes)."""
     th, X, dY, _ = _inputs(n, m, seed=n)

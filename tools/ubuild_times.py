@@ -19,6 +19,6 @@ for n in [int(v) for v in (sys.argv[1:] or ["256", "512", "1024", "1120", "2000"
     for _ in range(reps):
         e[0].record(); fwd(); e[1].record(); bwd(); e[2].record(); torch.cuda.synchronize()
         tf += e[0].elapsed_time(e[1]); tb += e[1].elapsed_time(e[2])
-    out[n] = {"build_U_ms": tf / reps, "grad_ms": tb / reps, "path": "ring" if n in (256, 512, 1024, 2047, 2048, 4095, 4096) else "generic"}
+    out[n] = {"build_U_ms": tf / reps, "grad_ms": tb / reps}
     print(n, out[n], flush=True)
 print(json.dumps(out))
