@@ -52,6 +52,10 @@ def lib():
         L.oracle_backward.argtypes = [ctypes.c_int, ctypes.c_int64, P, P, P, P, P, P]
         L.oracle_alg3.restype = ctypes.c_int
         L.oracle_alg3.argtypes = [ctypes.c_int, P, P, P, P, P]
+        L.oracle_u_apply.restype = ctypes.c_int
+        L.oracle_u_apply.argtypes = [ctypes.c_int, ctypes.c_int64, P, P, P, P, P, ctypes.c_int]
+        L.oracle_u_backward.restype = ctypes.c_int
+        L.oracle_u_backward.argtypes = [ctypes.c_int, ctypes.c_int64, P, P, P, P, P, P, P, P]
         _lib = L
     return _lib
 
@@ -167,3 +171,50 @@ def mask_from_keep(n: int, m_keep: int) -> np.ndarray:
     (both ends in S-bar = {m_keep..n-1}). Returns uint8 mask in flat angle order."""
     E = sequence_E(n)
     return (E[:, 0] < m_keep).astype(np.uint8)
+
+
+# ---------------------------------------------------------------- unitary U(n) (Appendix A)
+
+def _c2i(Z):
+    """complex128 n x m -> interleaved float64 n x 2m (re, im)."""
+    Z = np.ascontiguousarray(Z, dtype=np.complex128)
+    return Z.view(np.float64).reshape(Z.shape[0], 2 * Z.shape[1])
+
+
+def _i2c(A, m):
+    return np.ascontiguousarray(A).view(np.complex128).reshape(A.shape[0], m)
+
+
+def u_apply(n: int, theta, phi, X, mask=None, adjoint: bool = False):
+    """Y = U(theta, phi) X (Algorithm 4) or U^dagger X; X complex n x m."""
+    theta = np.ascontiguousarray(theta, dtype=np.float32)
+    phi = np.ascontiguousarray(phi, dtype=np.float32)
+    X = np.ascontiguousarray(X, dtype=np.complex128)
+    m = X.shape[1]
+    Xi = _c2i(X)
+    Yi = np.empty_like(Xi)
+    rc = lib().oracle_u_apply(n, m, _p(theta), _p(phi), _p(_mask_arg(mask, theta.size)), _p(Xi), _p(Yi),
+                              int(adjoint))
+    assert rc == 0
+    return _i2c(Yi, m)
+
+
+def u_build_U(n: int, theta, phi, mask=None):
+    return u_apply(n, theta, phi, np.eye(n, dtype=np.complex128), mask=mask)
+
+
+def u_backward(n: int, theta, phi, X, Gamma, mask=None, want_dX: bool = True):
+    """(dtheta, dphi, dX) for a real loss of Y = U X with Gamma = dL/dRe(Y) + i dL/dIm(Y)."""
+    theta = np.ascontiguousarray(theta, dtype=np.float32)
+    phi = np.ascontiguousarray(phi, dtype=np.float32)
+    X = np.ascontiguousarray(X, dtype=np.complex128)
+    m = X.shape[1]
+    N = num_angles(n)
+    Xi, Gi = _c2i(X), _c2i(Gamma)
+    dXi = np.empty_like(Xi) if want_dX else None
+    dth = np.zeros(N)
+    dph = np.zeros(N)
+    rc = lib().oracle_u_backward(n, m, _p(theta), _p(phi), _p(_mask_arg(mask, N)), _p(Xi), _p(Gi), _p(dXi),
+                                 _p(dth), _p(dph))
+    assert rc == 0
+    return dth, dph, (_i2c(dXi, m) if want_dX else None)

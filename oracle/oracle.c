@@ -311,3 +311,142 @@ int oracle_alg3(int n, const float *theta, const uint8_t *mask, const double *U,
     free(pairs); free(flat); free(Uf); free(M); free(A);
     return 0;
 }
+
+/* ======================================================================================
+ * Unitary U(n) (Appendix A). Complex matrices are interleaved (re, im)
+ * fp64, row-major. G^e(theta, phi) multiplies column i of the real Givens matrix by e^{i phi}
+ * (PAPER.md:199-201): G_ii = e^{i phi} cos, G_ij = -sin, G_ji = e^{i phi} sin, G_jj = cos --
+ * Algorithm 4's row update; the entry table at PAPER.md:973 also puts the
+ * phase on G_jj, which contradicts Alg. 4, dG/dtheta and the two-entry dG/dphi
+ * (PAPER.md:1030); we follow Alg. 4 (reading R15).
+ * Loss convention for a real loss L of complex U/Y (reading R16):
+ *   Gamma = dL/dRe(Y) + i dL/dIm(Y),  dL/dalpha = Re sum conj(Gamma) * dY/dalpha.
+ * ====================================================================================== */
+
+/* Algorithm 4 for the round-robin E on a copy of the complex n x m X:
+ * for e in reversed(E): r_i <- e^{i phi} cos U_i - sin U_j ; r_j <- e^{i phi} sin U_i + cos U_j.
+ * adjoint = 1 applies U^dagger = G^{e_N dagger} ... G^{e_1 dagger}: e in E order with
+ * G^dagger = [[e^{-i phi} c, e^{-i phi} s], [-s, c]]. */
+int oracle_u_apply(int n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const double *X,
+                   double *Y, int adjoint) {
+    if (n < 2 || m < 0) return -1;
+    int64_t N;
+    int32_t *E = build_E(n, &N);
+    memcpy(Y, X, sizeof(double) * 2 * (size_t)n * m);
+#pragma omp parallel for schedule(static)
+    for (int64_t col = 0; col < m; col++) {
+        for (int64_t q = 0; q < N; q++) {
+            int64_t e = adjoint ? q : (N - 1 - q);
+            if (mask && !mask[e]) continue;
+            int i = E[2 * e], j = E[2 * e + 1];
+            double c = cos((double)theta[e]), s = sin((double)theta[e]);
+            double pc = cos((double)phi[e]), ps = sin((double)phi[e]);
+            double *yi = Y + ((int64_t)i * m + col) * 2, *yj = Y + ((int64_t)j * m + col) * 2;
+            double ar = yi[0], ai = yi[1], br = yj[0], bi = yj[1];
+            if (!adjoint) {
+                double er = pc * ar - ps * ai, ei = pc * ai + ps * ar; /* e^{i phi} a */
+                yi[0] = c * er - s * br;
+                yi[1] = c * ei - s * bi;
+                yj[0] = s * er + c * br;
+                yj[1] = s * ei + c * bi;
+            } else {
+                double tr = c * ar + s * br, ti = c * ai + s * bi; /* row i of G^T applied */
+                yi[0] = pc * tr + ps * ti;                         /* e^{-i phi} (t) */
+                yi[1] = pc * ti - ps * tr;
+                yj[0] = -s * ar + c * br;
+                yj[1] = -s * ai + c * bi;
+            }
+        }
+    }
+    free(E);
+    return 0;
+}
+
+/* Backward of Y = U(theta, phi) X for a real loss with upstream Gamma (complex n x m):
+ * dtheta[e], dphi[e] = Re sum_cols conj(Gamma-propagated) * dY/d(.), and dX = U^dagger Gamma.
+ * Per column: run Algorithm 4 storing each rotation's complex inputs (a_i, a_j) (the tape);
+ * reverse sweep with the chain rule on y_i = e^{i phi}(c a_i) - s a_j, y_j = e^{i phi}(s a_i) + c a_j:
+ *   dy_i/dtheta = -e^{i phi} s a_i - c a_j,  dy_j/dtheta = e^{i phi} c a_i - s a_j,
+ *   dy_i/dphi = i e^{i phi} c a_i,           dy_j/dphi = i e^{i phi} s a_i,
+ *   g_a_i = conj(e^{i phi}) (c g_i + s g_j),  g_a_j = -s g_i + c g_j   (adjoint of the 2x2 map). */
+int oracle_u_backward(int n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const double *X,
+                      const double *G, double *dX, double *dtheta, double *dphi) {
+    if (n < 2 || m < 0) return -1;
+    int64_t N;
+    int32_t *E = build_E(n, &N);
+    int nt = oracle_num_threads();
+    double *pt = (double *)calloc((size_t)nt * N, sizeof(double));
+    double *pp = (double *)calloc((size_t)nt * N, sizeof(double));
+#pragma omp parallel num_threads(nt)
+    {
+        int t = 0;
+#ifdef _OPENMP
+        t = omp_get_thread_num();
+#endif
+        int64_t c0 = m * t / nt, c1 = m * (t + 1) / nt;
+        double *at = pt + (int64_t)t * N, *ap = pp + (int64_t)t * N;
+        double *x = (double *)malloc(sizeof(double) * 2 * n);
+        double *g = (double *)malloc(sizeof(double) * 2 * n);
+        double *tape = (double *)malloc(sizeof(double) * 4 * (size_t)N);
+        for (int64_t col = c0; col < c1; col++) {
+            for (int r = 0; r < n; r++) {
+                x[2 * r] = X[((int64_t)r * m + col) * 2];
+                x[2 * r + 1] = X[((int64_t)r * m + col) * 2 + 1];
+            }
+            for (int64_t e = N - 1; e >= 0; e--) {
+                if (mask && !mask[e]) continue;
+                int i = E[2 * e], j = E[2 * e + 1];
+                double c = cos((double)theta[e]), s = sin((double)theta[e]);
+                double pc = cos((double)phi[e]), ps = sin((double)phi[e]);
+                double ar = x[2 * i], ai = x[2 * i + 1], br = x[2 * j], bi = x[2 * j + 1];
+                tape[4 * e] = ar; tape[4 * e + 1] = ai; tape[4 * e + 2] = br; tape[4 * e + 3] = bi;
+                double er = pc * ar - ps * ai, ei = pc * ai + ps * ar;
+                x[2 * i] = c * er - s * br;
+                x[2 * i + 1] = c * ei - s * bi;
+                x[2 * j] = s * er + c * br;
+                x[2 * j + 1] = s * ei + c * bi;
+            }
+            for (int r = 0; r < n; r++) {
+                g[2 * r] = G[((int64_t)r * m + col) * 2];
+                g[2 * r + 1] = G[((int64_t)r * m + col) * 2 + 1];
+            }
+            for (int64_t e = 0; e < N; e++) {
+                if (mask && !mask[e]) continue;
+                int i = E[2 * e], j = E[2 * e + 1];
+                double c = cos((double)theta[e]), s = sin((double)theta[e]);
+                double pc = cos((double)phi[e]), ps = sin((double)phi[e]);
+                double ar = tape[4 * e], ai = tape[4 * e + 1], br = tape[4 * e + 2], bi = tape[4 * e + 3];
+                double er = pc * ar - ps * ai, ei = pc * ai + ps * ar; /* e^{i phi} a_i */
+                double gir = g[2 * i], gii = g[2 * i + 1], gjr = g[2 * j], gji = g[2 * j + 1];
+                /* dy/dtheta */
+                double yti_r = -s * er - c * br, yti_i = -s * ei - c * bi;
+                double ytj_r = c * er - s * br, ytj_i = c * ei - s * bi;
+                at[e] += gir * yti_r + gii * yti_i + gjr * ytj_r + gji * ytj_i; /* Re conj(g) dy */
+                /* dy/dphi = i e^{i phi} (c a_i, s a_i) */
+                double ypi_r = -c * ei, ypi_i = c * er;
+                double ypj_r = -s * ei, ypj_i = s * er;
+                ap[e] += gir * ypi_r + gii * ypi_i + gjr * ypj_r + gji * ypj_i;
+                /* adjoint of the 2x2 map */
+                double hr = c * gir + s * gjr, hi = c * gii + s * gji;
+                g[2 * i] = pc * hr + ps * hi;
+                g[2 * i + 1] = pc * hi - ps * hr;
+                g[2 * j] = -s * gir + c * gjr;
+                g[2 * j + 1] = -s * gii + c * gji;
+            }
+            if (dX)
+                for (int r = 0; r < n; r++) {
+                    dX[((int64_t)r * m + col) * 2] = g[2 * r];
+                    dX[((int64_t)r * m + col) * 2 + 1] = g[2 * r + 1];
+                }
+        }
+        free(x); free(g); free(tape);
+    }
+    for (int64_t e = 0; e < N; e++) {
+        double st = 0.0, sp = 0.0;
+        for (int t = 0; t < nt; t++) { st += pt[(int64_t)t * N + e]; sp += pp[(int64_t)t * N + e]; }
+        dtheta[e] = (mask && !mask[e]) ? 0.0 : st;
+        dphi[e] = (mask && !mask[e]) ? 0.0 : sp;
+    }
+    free(pt); free(pp); free(E);
+    return 0;
+}
