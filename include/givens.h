@@ -53,7 +53,8 @@ typedef enum {
     GIVENS_EUNSUPPORTED = -3  /* valid arguments but no kernel configuration for this n yet */
 } givens_status_t;
 
-enum { GIVENS_OP_APPLY = 0, GIVENS_OP_BUILD_U = 1, GIVENS_OP_BACKWARD = 2 };
+enum { GIVENS_OP_APPLY = 0, GIVENS_OP_BUILD_U = 1, GIVENS_OP_BACKWARD = 2,
+       GIVENS_OP_U_APPLY = 3, GIVENS_OP_U_BUILD_U = 4, GIVENS_OP_U_BACKWARD = 5 };
 enum { GIVENS_FLAG_RECOMPUTE = 1 };
 
 /* Thread-local description of the last failure ("" if none). */
@@ -82,7 +83,8 @@ int givens_schedule(int32_t n, int32_t *pairs_host, int64_t *flat_host);
  */
 int givens_mask_from_dims(int32_t n, const uint8_t *excluded_dims_host, uint8_t *mask_host);
 
-/* Workspace bytes for op (GIVENS_OP_*) at (n, m). Returns 0 for invalid arguments. */
+/* Workspace bytes for op (GIVENS_OP_*) at (n, m) (m = complex columns for the GIVENS_OP_U_*
+ * ops). Returns 0 for invalid arguments. */
 size_t givens_workspace_bytes(int op, int32_t n, int64_t m);
 
 /*
@@ -121,6 +123,38 @@ int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mas
  * givens_backward). Bit-exact against the schedule (pins the on-device indexing).
  */
 int givens_index_trace(int32_t n, int direction, int32_t *out_dev, void *stream);
+
+/* ------------------------------------------------------------------------------------------
+ * Unitary U(n) variant (Appendix A). theta, phi: fp32[N] in the same flat
+ * order; G^e(theta, phi) = R(theta) diag(e^{i phi}, 1) on (i, j), i.e. Algorithm 4's row update
+ * (r_i = e^{i phi} cos U_i - sin U_j, r_j = e^{i phi} sin U_i + cos U_j;
+ * DESIGN.md reading R15). Complex matrices are interleaved (re, im) fp32 pairs (complex64),
+ * row-major, leading dimensions in complex elements. Same workspace / stream / error rules as
+ * above, with the GIVENS_OP_U_* workspace ops. givens_u_supported(n) is 1 for 2 <= n <= 32768:
+ * n whose real ring configuration fits the unitary tables run on a register ring (one complex
+ * column per packed register pair), the rest (W = 32 rings, S = 2048, and the n without a ring)
+ * on the generic any-n kernel.
+ * ------------------------------------------------------------------------------------------ */
+int givens_u_supported(int32_t n);
+
+/* Y = U(theta, phi) X (adjoint = 0) or U^dagger X (adjoint = 1); X, Y complex n x m. */
+int givens_u_apply(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
+                   const float *X, int64_t ldx, float *Y, int64_t ldy, int adjoint,
+                   void *ws, size_t ws_bytes, void *stream);
+
+/* U = U(theta, phi), complex n x n (Algorithm 4 from U <- I_n). */
+int givens_u_build_U(int32_t n, const float *theta, const float *phi, const uint8_t *mask, float *U,
+                     int64_t ldu, void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * Backward for a real loss of Y = U X: dY = dL/dRe(Y) + i dL/dIm(Y) (complex n x m).
+ * dtheta[N], dphi[N] = dL/dtheta, dL/dphi (overwritten; masked entries 0), dX = U^dagger dY
+ * (optional). Replay by the adjoint rotations; per block the theta term uses Q_e and the phi term
+ * P_e, both reduced over the m columns deterministically.
+ */
+int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
+                      const float *Y, int64_t ldy, const float *dY, int64_t lddy, float *dX, int64_t lddx,
+                      float *dtheta, float *dphi, int flags, void *ws, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

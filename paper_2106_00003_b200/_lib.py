@@ -13,12 +13,14 @@ LIB_PATH = os.path.join(HERE, "libgivens.so")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, -1, -2, -3
 OP_APPLY, OP_BUILD_U, OP_BACKWARD = 0, 1, 2
+OP_U_APPLY, OP_U_BUILD_U, OP_U_BACKWARD = 3, 4, 5
 FLAG_RECOMPUTE = 1
 
 EXPORTS = [
     "givens_last_error", "givens_version", "givens_num_angles", "givens_supported",
     "givens_schedule", "givens_mask_from_dims", "givens_workspace_bytes", "givens_apply",
-    "givens_build_U", "givens_backward", "givens_index_trace",
+    "givens_build_U", "givens_backward", "givens_index_trace", "givens_u_supported", "givens_u_apply",
+    "givens_u_build_U", "givens_u_backward",
 ]
 
 
@@ -60,6 +62,14 @@ def lib():
         L.givens_backward.argtypes = [I32, I64, P, P, P, I64, P, I64, P, I64, P, C, P, SZ, P]
         L.givens_index_trace.restype = C
         L.givens_index_trace.argtypes = [I32, C, P, P]
+        L.givens_u_supported.restype = C
+        L.givens_u_supported.argtypes = [I32]
+        L.givens_u_apply.restype = C
+        L.givens_u_apply.argtypes = [I32, I64, P, P, P, P, I64, P, I64, C, P, SZ, P]
+        L.givens_u_build_U.restype = C
+        L.givens_u_build_U.argtypes = [I32, P, P, P, P, I64, P, SZ, P]
+        L.givens_u_backward.restype = C
+        L.givens_u_backward.argtypes = [I32, I64, P, P, P, P, I64, P, I64, P, I64, P, P, C, P, SZ, P]
         _lib = L
     return _lib
 

@@ -50,14 +50,16 @@ constexpr int kNW = GK_BWD_WARPS;  // warps per CTA of the backward ring kernel
 #define GK_FWD_WARPS 8
 #endif
 constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose ring kernels
-__host__ __device__ constexpr int ring_warps(int mode) { return mode == 3 ? kNW : kNWF; }
+__host__ __device__ constexpr int ring_warps(int mode) { return (mode & 3) == 3 ? kNW : kNWF; }
 
-enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3 };
+// base modes; M_UNI marks the unitary U(n) variant (Appendix A): complex columns stored as
+// interleaved (re, im) pairs, i.e. two real columns per complex column
+enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4 };
 
 __host__ __device__ constexpr int kcols(int W, int mode) {
-    // columns per thread, so that the column state is ~128 registers (2 W K forward, 4 W K
-    // backward); two packed fp32 columns per FFMA2
-    return (mode == M_BWD) ? (32 / W > 8 ? 8 : 32 / W) : (64 / W > 8 ? 8 : 64 / W);
+    // real columns per thread, so that the column state is ~128 registers (2 W K forward, 4 W K
+    // backward); two packed fp32 columns per FFMA2 (one complex column in the unitary variant)
+    return ((mode & 3) == M_BWD) ? (32 / W > 8 ? 8 : 32 / W) : (64 / W > 8 ? 8 : 64 / W);
 }
 
 // ------------------------------------------------------------------ PTX helpers
@@ -115,9 +117,11 @@ struct RingArgs {
     int64_t lddy;
     float *Y;         // FWD/BUILDU/TRANS: output; BWD: dX (nullable)
     int64_t ldy;
-    const uint8_t *coef;
+    const uint8_t *coef;     // (t, s) per slot, lane-chunked rows
+    const uint8_t *coef_ph;  // unitary: (p_t, q_t, p_b, q_b) phase factors per slot
+    const uint8_t *coef_ab;  // unitary backward: (alpha, beta) dphi weights per slot
     const uint8_t *sfin;
-    float *partial;   // BWD: [grid][2S][S] in chunk order (see chunk_pos)
+    float *partial;   // BWD: per CTA, per reduction group, NW warp blocks (see red_geom)
     int64_t nslabs;
     int vec_ok;       // 1 if all row starts are 16-byte aligned for K-wide vector access
 };
@@ -243,9 +247,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 struct RedGeom {
     int LW, H, NCHW, NSUM, OUTCH, RG, NW;
 };
-__host__ __device__ constexpr RedGeom red_geom(int W, int L) {
-    int LW = L < 32 ? L : 32, H = L / LW, NCHW = (W / 4) * LW, NSUM = kNW / H;
-    int RG = (NCHW >= 256 || (H > 1 && NCHW >= 128) || kNW > 8) ? 2 : 4;
+__host__ __device__ constexpr RedGeom red_geom(int W, int L, int vals = 1) {
+    int LW = L < 32 ? L : 32, H = L / LW, NCHW = (W / 4) * LW * vals, NSUM = kNW / H;
+    int RG = (NCHW >= 256 || (H > 1 && NCHW >= 128) || kNW > 8 || vals > 1) ? 2 : 4;
     return RedGeom{LW, H, NCHW, NSUM, (NCHW + NSUM - 1) / NSUM, RG, kNW};
 }
 
@@ -253,34 +257,40 @@ __host__ __device__ constexpr RedGeom red_geom(int W, int L) {
 // (L < 32: several groups per warp; L = 32 H: a group spans H warps).
 template <int W, int L, int MODE>
 struct RingGeom {
-    static constexpr int S = W * L;                 // slots = n_eff / 2
-    static constexpr int STEPS = 2 * S;             // pad + the R = 2S-1 blocks
+    static constexpr int S = W * L;                 // slots = n_eff / 2 (instantiated maximum)
     static constexpr int LW = L < 32 ? L : 32;      // lanes of a group inside one warp
     static constexpr int H = L / LW;                // warps per column group
     static constexpr int LC = 32 / LW;              // column groups per warp
+    static constexpr int BM = MODE & 3;             // base mode
+    static constexpr bool UNI = (MODE & M_UNI) != 0;
     static constexpr int NW = ring_warps(MODE);      // warps per CTA
     static constexpr int NGRP = NW * LC / H;        // column groups per CTA
-    static constexpr int K = kcols(W, MODE);        // columns per thread
-    static constexpr bool GRAD = (MODE == M_BWD);
+    static constexpr int K = kcols(W, MODE);        // real columns per thread
+    static constexpr bool GRAD = (BM == M_BWD);
     static constexpr int KP = (K + 1) / 2;          // packed register pairs per slot
-    // table rows per TMA stage: a power of two dividing W/2 with a stage of at most 16 KB
-    static constexpr int sps_pick() {  // stages of <= 32 KB forward, <= 16 KB next to the dtheta ring
+    // table bytes per slot staged per block: (t, s) 8 B; unitary adds the phases (16 B) and, in
+    // the backward, the dphi weights (alpha, beta) (8 B)
+    static constexpr int RB = 8 + (UNI ? 16 : 0) + ((UNI && GRAD) ? 8 : 0);
+    // table rows per TMA stage: a power of two dividing W/2, stages of <= 32 KB forward and
+    // <= 16 KB next to the dtheta ring
+    static constexpr int sps_pick() {
         int v = W / 2;
-        while (v > 1 && v * S * 8 > ((MODE == M_BWD) ? 16384 : 32768)) v /= 2;
+        while (v > 1 && v * S * RB > (GRAD ? 16384 : 32768)) v /= 2;
         return v;
     }
     static constexpr int SPS = sps_pick();
-    static constexpr int ROWB = S * 8;              // bytes per table row
-    static constexpr int STAGEB = SPS * ROWB;
+    static constexpr int STAGEB = SPS * S * RB;
     // stages in flight: 64 KB of table buffers next to the backward's dtheta ring, 96 KB otherwise
     static constexpr int NSTAGE_ = (GRAD ? 65536 : 98304) / STAGEB;
     static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
-    // backward dtheta sums: per-warp ring of NG groups of RG steps, reduced one group later
-    static constexpr int RG = red_geom(W, L).RG;     // steps per reduction group
+    // backward sums (dtheta, and dphi in the unitary variant): per-warp ring of NG groups of RG
+    // steps, reduced one group later
+    static constexpr int VALS = UNI ? 2 : 1;
+    static constexpr int RG = red_geom(W, L, VALS).RG;  // steps per reduction group
     static constexpr int NG = 2;                    // groups in flight
     static constexpr int D = RG * NG;               // ring depth in steps
-    static constexpr int NCH = S / 4;               // float4 chunks of a step's per-slot sums
-    static constexpr int NCHW = (W / 4) * LW;       // chunks held by one warp (= NCH / H)
+    static constexpr int NCHW1 = (W / 4) * LW;      // dtheta chunks held by one warp
+    static constexpr int NCHW = NCHW1 * VALS;       // all chunks of a warp's ring row
     static constexpr int NSUM = NW / H;             // warps contributing to each chunk
     static constexpr int OUTCH = (NCHW + NSUM - 1) / NSUM;  // chunks reduced per warp (max)
     static constexpr int XV = GRAD ? 2 * KP : KP;   // packed values crossing a warp boundary per direction
@@ -290,6 +300,16 @@ struct RingGeom {
     static constexpr size_t OFF_OUT = OFF_RED + (GRAD ? (size_t)NW * D * NCHW * 16 : 0);
     static constexpr size_t SMEM = OFF_OUT + (GRAD ? (size_t)NW * NG * RG * OUTCH * 16 : 0);
 };
+
+// complex multiply of a packed (re, im) value by (p + i q), and by its conjugate (p - i q)
+__device__ __forceinline__ float2 cmul(float2 z, float p, float q) {
+    return __ffma2_rn(make_float2(z.y, z.y), make_float2(-q, p), __fmul2_rn(make_float2(z.x, z.x), make_float2(p, q)));
+}
+__device__ __forceinline__ float2 cmulc(float2 z, float p, float q) {
+    return __ffma2_rn(make_float2(z.y, z.y), make_float2(q, p), __fmul2_rn(make_float2(z.x, z.x), make_float2(p, -q)));
+}
+__device__ __forceinline__ float cmul(float z, float, float) { return z; }
+__device__ __forceinline__ float cmulc(float z, float, float) { return z; }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -315,12 +335,15 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     // (S = W * La with La in (L - 32, L]); buffers are sized for the instantiated maximum
     const int La = (H == 1 && LC > 1) ? L : a.La;
     const int S = W * La, STEPS = 2 * S;
-    const int rowb = S * 8;                       // bytes per table row
-    const uint32_t stage_bytes = (uint32_t)(SPS * rowb);
+    const int rowb = S * 8;                       // bytes per (t, s) table row
+    const uint32_t stage_bytes = (uint32_t)(SPS * S * G::RB);
     constexpr int RG = G::RG, NG = G::NG, D = G::D, NCHW = G::NCHW, NSUM = G::NSUM, OUTCH = G::OUTCH;
     constexpr int XV = G::XV;
     constexpr int NW = G::NW;
-    constexpr bool UP = (MODE == M_TRANS || MODE == M_BWD);  // walk b_1 -> b_R (inverse rotations)
+    constexpr int BM = G::BM;
+    constexpr bool UNI = G::UNI;
+    constexpr int NCHW1 = G::NCHW1;
+    constexpr bool UP = (BM == M_TRANS || BM == M_BWD);  // walk b_1 -> b_R (inverse rotations)
     constexpr bool GRAD = G::GRAD;
     static_assert(W % SPS == 0 && W % RG == 0 && W % 4 == 0 && W % 2 == 0, "geometry");
     static_assert(H == 1 || LW == 32, "multi-warp groups use whole warps");
@@ -371,17 +394,25 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             for (int i = 0; i < NG; i++) mbar_arrive(&rempty[i]);
     }
 
-    // table rows of slab-local stage j: forward reads rho = 2S - u (descending), backward rho = u
-    auto stage_src = [&](int gst) -> const uint8_t * {
+    // table rows of slab-local stage j: forward reads rho = 2S - u (descending), backward rho = u;
+    // a stage holds SPS rows of each staged table part: (t, s) [, phases [, (alpha, beta)]]
+    auto stage_rho0 = [&](int gst) -> int {
         int j = gst % (STEPS / SPS);
-        int rho0 = UP ? j * SPS : (STEPS - (j + 1) * SPS + 1);
-        return a.coef + (int64_t)rho0 * rowb;
+        return UP ? j * SPS : (STEPS - (j + 1) * SPS + 1);
+    };
+    auto issue_stage = [&](int gst, int b) {
+        const int rho0 = stage_rho0(gst);
+        uint8_t *dst = stagebuf + (size_t)b * G::STAGEB;
+        mbar_expect_tx(&full[b], stage_bytes);
+        bulk_g2s(dst, a.coef + (int64_t)rho0 * rowb, (uint32_t)(SPS * rowb), &full[b]);
+        if constexpr (UNI) {
+            bulk_g2s(dst + SPS * rowb, a.coef_ph + (int64_t)rho0 * 2 * rowb, (uint32_t)(SPS * 2 * rowb), &full[b]);
+            if constexpr (GRAD)
+                bulk_g2s(dst + SPS * 3 * rowb, a.coef_ab + (int64_t)rho0 * rowb, (uint32_t)(SPS * rowb), &full[b]);
+        }
     };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NSTAGE && s < total_stages; s++) {
-            mbar_expect_tx(&full[s], stage_bytes);
-            bulk_g2s(stagebuf + (size_t)s * G::STAGEB, stage_src(s), stage_bytes, &full[s]);
-        }
+        for (int s = 0; s < NSTAGE && s < total_stages; s++) issue_stage(s, s);
     }
 
     // dtheta stage 1: reduce ring group gg (steps gg*RG .. gg*RG+RG-1 of this CTA) over the NSUM
@@ -452,7 +483,14 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             else    { rt = row_s0(pt);       rb = row_s0(pb); }
             if (!active) rt = rb = n;  // idle lanes hold zeros and never store
             V vt[KP], vb[KP];
-            if constexpr (MODE == M_BUILDU) {
+            if constexpr (BM == M_BUILDU && UNI) {
+#pragma unroll
+                for (int p = 0; p < KP; p++) {  // one complex column per pack: 1 + 0i on the diagonal
+                    const int64_t c = (col0 >> 1) + p;
+                    vt[p] = make_float2((rt < n && c == rt) ? 1.f : 0.f, 0.f);
+                    vb[p] = make_float2((rb < n && c == rb) ? 1.f : 0.f, 0.f);
+                }
+            } else if constexpr (BM == M_BUILDU) {
 #pragma unroll
                 for (int p = 0; p < KP; p++) {
                     const int64_t c = col0 + 2 * p;
@@ -496,8 +534,11 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     mbar_wait(&full[gst % NSTAGE], (uint32_t)((gst / NSTAGE) & 1));
                     __syncwarp();
                 }
-                const float4 *row4 = reinterpret_cast<const float4 *>(
-                    stagebuf + (gst % NSTAGE) * G::STAGEB + (UP ? su : (SPS - 1 - su)) * rowb);
+                const int srow = UP ? su : (SPS - 1 - su);
+                const uint8_t *sbase = stagebuf + (gst % NSTAGE) * G::STAGEB;
+                const float4 *row4 = reinterpret_cast<const float4 *>(sbase + srow * rowb);
+                const float4 *ph4 = reinterpret_cast<const float4 *>(sbase + SPS * rowb + srow * 2 * rowb);
+                const float4 *ab4 = reinterpret_cast<const float4 *>(sbase + SPS * 3 * rowb + srow * rowb);
                 constexpr int r = uu % RG;
                 int bi = 0;
                 float4 *ring_dst = nullptr;
@@ -510,34 +551,70 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     ring_dst = red + ((size_t)warp * D + bi * RG + r) * NCHW;
                 }
                 float acc[GRAD ? (LC > 1 ? W : 4) : 1];
+                float accp[(GRAD && UNI) ? (LC > 1 ? W : 4) : 1];
 #pragma unroll
                 for (int pp = 0; pp < W / 2; pp++) {
                     const float4 cf = row4[pp * La + tc];
+                    float4 ab = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if constexpr (GRAD && UNI) ab = ab4[pp * La + tc];
 #pragma unroll
                     for (int hh = 0; hh < 2; hh++) {
                         const int q = 2 * pp + hh;
                         const float tq = hh ? cf.z : cf.x, sq = hh ? cf.w : cf.y;
+                        float4 ph = make_float4(1.f, 0.f, 1.f, 0.f);
+                        if constexpr (UNI) ph = ph4[q * La + tc];  // (p_t, q_t, p_b, q_b)
                         if constexpr (GRAD) {
                             // dtheta contribution before this block's inverse rotation:
-                            // dz_bottom * z_top - dz_top * z_bottom (Q_e structure)
+                            // dz_bottom * z_top - dz_top * z_bottom (Q_e structure, PAPER.md:515-521;
+                            // in the unitary variant Re(conj(dz_b) z_t - conj(dz_t) z_b), the same
+                            // sum over the (re, im) halves)
                             float c = cross_acc(0.f, DB[0][q], ZT[0][q], DT[0][q], ZB[0][q]);
 #pragma unroll
                             for (int p = 1; p < KP; p++) c = cross_acc(c, DB[p][q], ZT[p][q], DT[p][q], ZB[p][q]);
                             acc[LC > 1 ? q : (q & 3)] = c;
+                            if constexpr (UNI) {
+                                // dphi: Re(i conj(v) w), w = alpha z_t + beta z_b, v = alpha dz_t + beta dz_b
+                                // (P_e structure, in z-space)
+                                const float al = hh ? ab.z : ab.x, be = hh ? ab.w : ab.y;
+                                float cp = 0.f;
+#pragma unroll
+                                for (int p = 0; p < KP; p++) {
+                                    const V w = fma_v(be, ZB[p][q], mul_v(f2(al), ZT[p][q]));
+                                    const V v = fma_v(be, DB[p][q], mul_v(f2(al), DT[p][q]));
+                                    cp = phi_acc(cp, v, w);
+                                }
+                                accp[LC > 1 ? q : (q & 3)] = cp;
+                            }
                         }
 #pragma unroll
                         for (int p = 0; p < KP; p++) {
                             if (UP) {
                                 if constexpr (GRAD) rot_inv2(ZT[p][q], ZB[p][q], DT[p][q], DB[p][q], tq, sq);
                                 else rot_inv(ZT[p][q], ZB[p][q], tq, sq);
+                                if constexpr (UNI) {  // G^dagger = diag(conj phases) R^T
+                                    ZT[p][q] = cmulc(ZT[p][q], ph.x, ph.y);
+                                    ZB[p][q] = cmulc(ZB[p][q], ph.z, ph.w);
+                                    if constexpr (GRAD) {
+                                        DT[p][q] = cmulc(DT[p][q], ph.x, ph.y);
+                                        DB[p][q] = cmulc(DB[p][q], ph.z, ph.w);
+                                    }
+                                }
                             } else {
+                                if constexpr (UNI) {  // G = R diag(phases): phase first
+                                    ZT[p][q] = cmul(ZT[p][q], ph.x, ph.y);
+                                    ZB[p][q] = cmul(ZB[p][q], ph.z, ph.w);
+                                }
                                 rot_fwd(ZT[p][q], ZB[p][q], tq, sq);
                             }
                         }
                     }
                     if constexpr (GRAD && LC == 1) {
                         // one lane per column group and warp: the per-slot sums go straight to the ring
-                        if (pp & 1) ring_dst[(pp >> 1) * LW + tl] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                        if (pp & 1) {
+                            ring_dst[(pp >> 1) * LW + tl] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+                            if constexpr (UNI)
+                                ring_dst[NCHW1 + (pp >> 1) * LW + tl] = make_float4(accp[0], accp[1], accp[2], accp[3]);
+                        }
                     }
                 }
                 if constexpr (GRAD) {
@@ -545,13 +622,20 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
 #pragma unroll
                         for (int q = 0; q < W; q++) {
 #pragma unroll
-                            for (int o = LW; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                            for (int o = LW; o < 32; o <<= 1) {
+                                acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+                                if constexpr (UNI) accp[q] += __shfl_xor_sync(0xffffffffu, accp[q], o);
+                            }
                         }
                         if (g == 0) {
 #pragma unroll
-                            for (int q4 = 0; q4 < W / 4; q4++)
+                            for (int q4 = 0; q4 < W / 4; q4++) {
                                 ring_dst[q4 * LW + tl] =
                                     make_float4(acc[4 * q4], acc[4 * q4 + 1], acc[4 * q4 + 2], acc[4 * q4 + 3]);
+                                if constexpr (UNI)
+                                    ring_dst[NCHW1 + q4 * LW + tl] =
+                                        make_float4(accp[4 * q4], accp[4 * q4 + 1], accp[4 * q4 + 2], accp[4 * q4 + 3]);
+                            }
                         }
                     }
                     if constexpr (r == RG - 1) {
@@ -646,8 +730,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                             const int nxt = gst + NSTAGE;
                             if (nxt < total_stages) {
                                 fence_proxy_async_smem();
-                                mbar_expect_tx(&full[b], stage_bytes);
-                                bulk_g2s(stagebuf + (size_t)b * G::STAGEB, stage_src(nxt), stage_bytes, &full[b]);
+                                issue_stage(nxt, b);
                             }
                         }
                     }
@@ -658,7 +741,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         }
 
         // ---------------- store from the end layout (s_{R-1} forward, s_0 backward)
-        if (MODE == M_BWD && a.Y == nullptr) continue;
+        if (BM == M_BWD && a.Y == nullptr) continue;
 #pragma unroll
         for (int q = 0; q < W; q++) {
             const int k = t * W + q;

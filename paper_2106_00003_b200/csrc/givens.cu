@@ -109,6 +109,27 @@ Cfg make_cfg(int n) {
     return c;
 }
 
+// unitary variant: the ring kernels carry 16-24 more table bytes per slot, which rules out W = 32
+// (registers) and W * L > 1024 (shared memory); those n take an idle-lane ring if one fits, else
+// the generic kernel
+Cfg make_cfg_u(int n) {
+    Cfg c = make_cfg(n);
+    if (c.fast && (c.W == 32 || c.W * c.L > 1024)) {
+        c.fast = 0; c.W = c.S; c.L = 1; c.La = 1;
+        for (int w : {16, 8}) {
+            if (c.S % w == 0 && c.S / w >= 2 && c.S / w <= 128) {
+                int La = c.S / w, L = La <= 32 ? 32 : (La <= 64 ? 64 : 128);
+                if (w * L > 1024) continue;
+                c.fast = 1; c.W = w; c.La = La; c.L = L;
+                break;
+            }
+        }
+    }
+    return c;
+}
+
+Cfg cfg_for_op(int n, int op) { return op >= 3 ? make_cfg_u(n) : make_cfg(n); }
+
 int dev_sms() {
     static std::mutex mu;
     static int cache[64] = {0};
@@ -137,34 +158,41 @@ int64_t grid_for(const Cfg &c, int mode, int64_t m) {
 }
 
 struct WsLayout {
-    size_t coef, amap, flip, sig, sfin, partial, scratch, total;
+    size_t coef, coef_ph, coef_ab, amap, flip, sig, sfin, partial, scratch, total;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
+// ops 0..2: GIVENS_OP_*; 3..5: the unitary variants (m counts complex columns)
 WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
+    const bool uni = op >= 3;
+    const int base = op % 3;
+    const int64_t mr = uni ? 2 * m : m;  // real columns
     WsLayout L;
     size_t off = 0;
-    L.coef = off; off = al256(off + (size_t)(2 * c.S + 1) * c.rowbytes);
-    L.amap = off; off = al256(off + (size_t)(2 * c.S + 1) * c.S * 4);
+    const size_t rows = (size_t)(2 * c.S + 1);
+    L.coef = off; off = al256(off + rows * c.rowbytes);
+    L.coef_ph = off; if (uni) off = al256(off + rows * c.S * 16);
+    L.coef_ab = off; if (uni) off = al256(off + rows * c.S * 8);
+    L.amap = off; off = al256(off + rows * c.S * 4);
     L.flip = off; off = al256(off + (size_t)c.R * c.S);
     L.sig = off; off = al256(off + (size_t)c.R * c.ne);
     L.sfin = off; off = al256(off + (size_t)c.ne);
     L.partial = off;
-    if (op == GIVENS_OP_BACKWARD) {
-        int64_t g = grid_for(c, M_BWD, m);
-        size_t per_step = (size_t)c.S * 4;  // generic kernel: natural order
+    if (base == GIVENS_OP_BACKWARD) {
+        int64_t g = grid_for(c, M_BWD, mr);
+        size_t per_step = (size_t)c.S * 4 * (uni ? 2 : 1);  // generic kernel: natural order, [vals][2S][S]
         if (c.fast) {
-            const RedGeom rg = red_geom(c.W, c.L);
+            const RedGeom rg = red_geom(c.W, c.L, uni ? 2 : 1);
             per_step = (size_t)rg.NW * rg.OUTCH * 16;  // >= S floats (padded when chunks don't split evenly)
         }
         off = al256(off + (size_t)g * 2 * c.S * per_step);
     }
     L.scratch = off;
     if (!c.fast) {
-        int mode = op == GIVENS_OP_BACKWARD ? M_BWD : M_FWD;
-        int64_t g = grid_for(c, mode, m);
-        off = al256(off + (size_t)g * 32 * c.ne * (op == GIVENS_OP_BACKWARD ? 2 : 1) * 4);
+        int mode = base == GIVENS_OP_BACKWARD ? M_BWD : M_FWD;
+        int64_t g = grid_for(c, mode, mr);
+        off = al256(off + (size_t)g * 32 * c.ne * (base == GIVENS_OP_BACKWARD ? 2 : 1) * (uni ? 2 : 1) * 4);
     }
     L.total = off;
     return L;
@@ -263,11 +291,48 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
     amap[(int64_t)rho * S + k] = code;
 }
 
+// (3u) unitary tables (Appendix A): G^e = R(theta) diag(e^{i phi}, 1) on (i, j) (Alg. 4,
+// PAPER.md:1002-1005). In (top, bottom) ring coordinates the phase sits on whichever of the two
+// holds row i: ph[rho][slot] = (p_t, q_t, p_b, q_b) with (p, q) = (cos phi, sin phi) there and
+// (1, 0) on the other. ab[rho][slot] = (alpha, beta): the dphi weights, w = alpha z_t + beta z_b
+// = cos(th_r) z_i + sigma_i sigma_j sin(th_r) z_j, th_r the pi-reduced angle.
+__global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ theta, const float *__restrict__ phi,
+                         const uint8_t *__restrict__ mask, const uint8_t *__restrict__ sig, float4 *__restrict__ ph,
+                         float2 *__restrict__ ab) {
+    int S = ne / 2, R = ne - 1;
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (int64_t)(R + 2) * S) return;
+    int rho = (int)(idx / S), k = (int)(idx % S);
+    int t = k / W, q = k % W;
+    float4 *phr = ph + (int64_t)rho * S;
+    float2 *abr = ab + (int64_t)rho * S;
+    int pos_ph = q * L + t;          // one float4 per slot
+    int pos_ab = coef_pos(k, W, L);  // one float2 per slot, pairs of slots per float4
+    if (rho == 0 || rho == R + 1) {
+        phr[pos_ph] = make_float4(1.f, 0.f, 1.f, 0.f);
+        abr[pos_ab] = make_float2(0.f, 0.f);
+        return;
+    }
+    int r = rho - 1;
+    int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);
+    int64_t f = flat_of(r, k, n, ne);
+    bool active = f >= 0 && (!mask || mask[f]);
+    double th = active ? (double)theta[f] : 0.0, pv = active ? (double)phi[f] : 0.0;
+    double thr = th;
+    if (fabs(th) > 1.5707963267948966) thr = th - copysign(3.141592653589793, th);
+    float pc = (float)cos(pv), ps = (float)sin(pv);
+    bool top_is_i = a < b;
+    phr[pos_ph] = top_is_i ? make_float4(pc, ps, 1.f, 0.f) : make_float4(1.f, 0.f, pc, ps);
+    double cr = cos(thr), sr = sin(thr);
+    if (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) sr = -sr;
+    abr[pos_ab] = top_is_i ? make_float2((float)cr, (float)sr) : make_float2((float)sr, (float)cr);
+}
+
 // ------------------------------------------------------------------ stage-2 dtheta reduction
 // dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in fixed CTA order (PAPER.md:768-781
 // "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0.
-__global__ void k_dtheta_reduce(int S, int W, int L, int G, int ring, const float *__restrict__ partial,
-                                const int32_t *__restrict__ amap, float *__restrict__ dtheta) {
+__global__ void k_dtheta_reduce(int S, int W, int L, int G, int ring, int vals, const float *__restrict__ partial,
+                                const int32_t *__restrict__ amap, float *__restrict__ dtheta, float *__restrict__ dphi) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int rows = 2 * S;
     if (idx >= (int64_t)rows * S) return;
@@ -276,32 +341,37 @@ __global__ void k_dtheta_reduce(int S, int W, int L, int G, int ring, const floa
     int64_t f = code & 0x1FFFFFFF;
     if (code & (1 << 29)) {
         dtheta[f] = 0.f;
+        if (vals > 1) dphi[f] = 0.f;
         return;
     }
     int rho = (int)(idx / S), k = (int)(idx % S);
-    int64_t pos, stride;
-    if (ring) {
-        // ring kernel layout: per CTA, per group of RG steps, NW warp blocks of RG x OUTCH float4;
-        // slot k (lane t = k / W of the group, slot q = k % W) is chunk ci = (q/4)*LW + t%LW of the
-        // warp slice t/LW, reduced by the warp c*H + slice that owns ci
-        const RedGeom rg = red_geom(W, L);
-        int t = k / W, q = k % W, hs = t / rg.LW, tl = t % rg.LW;
-        int ci = (q >> 2) * rg.LW + tl;
-        int c = 0;
-        while (c + 1 < rg.NSUM && ((c + 1) * rg.NCHW) / rg.NSUM <= ci) c++;
-        int j = ci - (c * rg.NCHW) / rg.NSUM;
-        int w = c * rg.H + hs;
-        int64_t blk = ((int64_t)(rho / rg.RG) * rg.NW + w) * rg.RG * rg.OUTCH;
-        pos = (blk + (rho % rg.RG) * rg.OUTCH + j) * 4 + (q & 3);
-        stride = (int64_t)rows * rg.NW * rg.OUTCH * 4;
-    } else {
-        pos = (int64_t)rho * S + k;  // generic kernel: natural order
-        stride = (int64_t)rows * S;
+    for (int v = 0; v < vals; v++) {
+        int64_t pos, stride;
+        if (ring) {
+            // ring kernel layout: per CTA, per group of RG steps, NW warp blocks of RG x OUTCH float4;
+            // slot k (lane t = k / W of the group, slot q = k % W) is chunk ci = v*NCHW1 + (q/4)*LW + t%LW
+            // of the warp slice t/LW (v = 0: dtheta, 1: dphi), reduced by the warp c*H + slice owning ci
+            const RedGeom rg = red_geom(W, L, vals);
+            const int nchw1 = rg.NCHW / vals;
+            int t = k / W, q = k % W, hs = t / rg.LW, tl = t % rg.LW;
+            int ci = v * nchw1 + (q >> 2) * rg.LW + tl;
+            int c = 0;
+            while (c + 1 < rg.NSUM && ((c + 1) * rg.NCHW) / rg.NSUM <= ci) c++;
+            int j = ci - (c * rg.NCHW) / rg.NSUM;
+            int w = c * rg.H + hs;
+            int64_t blk = ((int64_t)(rho / rg.RG) * rg.NW + w) * rg.RG * rg.OUTCH;
+            pos = (blk + (rho % rg.RG) * rg.OUTCH + j) * 4 + (q & 3);
+            stride = (int64_t)rows * rg.NW * rg.OUTCH * 4;
+        } else {
+            pos = ((int64_t)v * rows + rho) * S + k;  // generic kernel: natural order, [vals][rows][S]
+            stride = (int64_t)vals * rows * S;
+        }
+        float s = 0.f;
+        const float *p = partial + pos;
+        for (int cc = 0; cc < G; cc++) s += p[(int64_t)cc * stride];
+        if (v == 0) dtheta[f] = (code & (1 << 30)) ? -s : s;
+        else dphi[f] = s;  // dphi carries no sign: sigma_i^2 = 1
     }
-    float s = 0.f;
-    const float *p = partial + pos;
-    for (int cc = 0; cc < G; cc++) s += p[(int64_t)cc * stride];
-    dtheta[f] = (code & (1 << 30)) ? -s : s;
 }
 
 // ------------------------------------------------------------------ generic any-n kernel
@@ -316,9 +386,11 @@ struct GenArgs {
     const float *dY; int64_t lddy;
     float *Y; int64_t ldy;
     const uint8_t *coef;
+    const float4 *coef_ph;  // unitary: phases per slot, natural order
+    const float2 *coef_ab;  // unitary backward: dphi weights per slot, natural order
     const uint8_t *sfin;
     float *partial;
-    float *scratch;  // [ne][G*32] (Z) and, for BWD, another [ne][G*32] (D)
+    float *scratch;  // [ne][G*32] (Z) and, for BWD, another [ne][G*32] (D); float2 entries when unitary
     int64_t nslabs;
 };
 
@@ -386,6 +458,101 @@ __global__ void __launch_bounds__(32) k_generic(const GenArgs a) {
     if (GRAD && slab_i == 0) {
         // CTA without slabs: zero its partial so stage 2 can sum every CTA
         for (int64_t i = lane; i < (int64_t)steps * S; i += 32) a.partial[(int64_t)blockIdx.x * steps * S + i] = 0.f;
+    }
+}
+
+// Unitary variant of k_generic (Appendix A, Alg. 4): one complex column per thread, the same
+// table conventions as the ring's unitary path (k_coef_u), dtheta and dphi partials per CTA as
+// [2][2S][S] (dtheta, then dphi). a.m counts real columns (2 per complex column).
+template <int BM>
+__global__ void __launch_bounds__(32) k_generic_u(const GenArgs a) {
+    constexpr bool UP = (BM == M_TRANS || BM == M_BWD);
+    constexpr bool GRAD = (BM == M_BWD);
+    const int lane = threadIdx.x;
+    const int ne = a.ne, n = a.n, S = a.S;
+    const int steps = 2 * S;
+    const int64_t mc = a.m / 2;
+    const int64_t stride = (int64_t)gridDim.x * 32;
+    float2 *Z = reinterpret_cast<float2 *>(a.scratch) + (int64_t)blockIdx.x * 32 + lane;
+    float2 *D = Z + (int64_t)ne * stride;
+    int64_t slab_i = 0;
+    for (int64_t slab = blockIdx.x; slab < a.nslabs; slab += gridDim.x, slab_i++) {
+        const int64_t col = slab * 32 + lane;
+        const bool live = col < mc;
+        for (int i = 0; i < ne; i++) {
+            float2 v = make_float2(0.f, 0.f), d = make_float2(0.f, 0.f);
+            if (i < n && live) {
+                if (BM == M_BUILDU) v.x = (col == i) ? 1.f : 0.f;
+                else v = make_float2(a.X[(int64_t)i * a.ldx + 2 * col], a.X[(int64_t)i * a.ldx + 2 * col + 1]);
+                if (GRAD) d = make_float2(a.dY[(int64_t)i * a.lddy + 2 * col], a.dY[(int64_t)i * a.lddy + 2 * col + 1]);
+                if (UP && a.sfin[i]) { v = neg_v(v); d = neg_v(d); }
+            }
+            Z[(int64_t)i * stride] = v;
+            if (GRAD) D[(int64_t)i * stride] = d;
+        }
+        for (int u = 0; u < steps; u++) {
+            int rho = UP ? u : (steps - u);
+            if (rho == 0 || rho == steps) continue;  // pad rows are the identity
+            int r = rho - 1;
+            const float2 *row = reinterpret_cast<const float2 *>(a.coef + (int64_t)rho * a.rowbytes);
+            for (int k = 0; k < S; k++) {
+                int rt = seq_at(r, k, ne), rbm = seq_at(r, ne - 1 - k, ne);
+                const float2 cf = row[k];
+                const float4 ph = a.coef_ph[(int64_t)rho * S + k];  // (p_t, q_t, p_b, q_b)
+                float2 x = Z[(int64_t)rt * stride], y = Z[(int64_t)rbm * stride];
+                if (GRAD) {
+                    float2 dx = D[(int64_t)rt * stride], dy = D[(int64_t)rbm * stride];
+                    const float2 ab = a.coef_ab[(int64_t)rho * S + k];
+                    // dtheta: Re(conj(dz_b) z_t - conj(dz_t) z_b); dphi: Re(i conj(v) w) with
+                    // w = alpha z_t + beta z_b, v = alpha dz_t + beta dz_b
+                    float vt = 0.f, vp = 0.f;
+                    if (live) {
+                        vt = dy.x * x.x + dy.y * x.y - dx.x * y.x - dx.y * y.y;
+                        float2 w = make_float2(ab.x * x.x + ab.y * y.x, ab.x * x.y + ab.y * y.y);
+                        float2 v = make_float2(ab.x * dx.x + ab.y * dy.x, ab.x * dx.y + ab.y * dy.y);
+                        vp = v.y * w.x - v.x * w.y;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        vt += __shfl_xor_sync(0xffffffffu, vt, o);
+                        vp += __shfl_xor_sync(0xffffffffu, vp, o);
+                    }
+                    if (lane == 0) {
+                        float *pt = a.partial + (((int64_t)blockIdx.x * 2 + 0) * steps + rho) * S + k;
+                        float *pp = a.partial + (((int64_t)blockIdx.x * 2 + 1) * steps + rho) * S + k;
+                        *pt = (slab_i > 0) ? (*pt + vt) : vt;
+                        *pp = (slab_i > 0) ? (*pp + vp) : vp;
+                    }
+                    rot_inv(dx, dy, cf.x, cf.y);
+                    dx = cmulc(dx, ph.x, ph.y);
+                    dy = cmulc(dy, ph.z, ph.w);
+                    D[(int64_t)rt * stride] = dx;
+                    D[(int64_t)rbm * stride] = dy;
+                }
+                if (UP) {  // G^dagger = diag(conj phases) R^T
+                    rot_inv(x, y, cf.x, cf.y);
+                    x = cmulc(x, ph.x, ph.y);
+                    y = cmulc(y, ph.z, ph.w);
+                } else {  // G = R diag(phases)
+                    x = cmul(x, ph.x, ph.y);
+                    y = cmul(y, ph.z, ph.w);
+                    rot_fwd(x, y, cf.x, cf.y);
+                }
+                Z[(int64_t)rt * stride] = x;
+                Z[(int64_t)rbm * stride] = y;
+            }
+        }
+        if (live && !(GRAD && a.Y == nullptr)) {
+            for (int i = 0; i < n; i++) {
+                float2 v = GRAD ? D[(int64_t)i * stride] : Z[(int64_t)i * stride];
+                if (!UP && a.sfin[i]) v = neg_v(v);
+                a.Y[(int64_t)i * a.ldy + 2 * col] = v.x;
+                a.Y[(int64_t)i * a.ldy + 2 * col + 1] = v.y;
+            }
+        }
+    }
+    if (GRAD && slab_i == 0) {
+        for (int64_t i = lane; i < (int64_t)2 * steps * S; i += 32) a.partial[(int64_t)blockIdx.x * 2 * steps * S + i] = 0.f;
     }
 }
 
@@ -509,7 +676,7 @@ int launch_ring(int mode, const Cfg &c, RingArgs &ra, int64_t grid, cudaStream_t
 }
 
 int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask, uint8_t *ws, const WsLayout &L,
-                   cudaStream_t st) {
+                   cudaStream_t st, const float *phi = nullptr) {
     int64_t RS = (int64_t)c.R * c.S;
     k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, ws + L.flip);
     CUDA_TRY(cudaGetLastError());
@@ -521,6 +688,12 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
                                                           ws + L.sig, ws + L.coef,
                                                           reinterpret_cast<int32_t *>(ws + L.amap));
     CUDA_TRY(cudaGetLastError());
+    if (phi) {
+        k_coef_u<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, theta, phi, mask, ws + L.sig,
+                                                                reinterpret_cast<float4 *>(ws + L.coef_ph),
+                                                                reinterpret_cast<float2 *>(ws + L.coef_ab));
+        CUDA_TRY(cudaGetLastError());
+    }
     return 0;
 }
 
@@ -553,6 +726,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
         ra.n = n; ra.ne = c.ne; ra.La = c.La;
         ra.m = m; ra.X = X; ra.ldx = ldx; ra.dY = dY; ra.lddy = lddy; ra.Y = Y; ra.ldy = ldy;
         ra.coef = ws + L.coef; ra.sfin = ws + L.sfin;
+        ra.coef_ph = ws + L.coef_ph; ra.coef_ab = ws + L.coef_ab;
         ra.partial = reinterpret_cast<float *>(ws + L.partial);
         ra.nslabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
         int K = kcols(c.W, mode);
@@ -563,14 +737,21 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
     ga.n = n; ga.ne = c.ne; ga.S = c.S; ga.rowbytes = c.rowbytes; ga.m = m;
     ga.X = X; ga.ldx = ldx; ga.dY = dY; ga.lddy = lddy; ga.Y = Y; ga.ldy = ldy;
     ga.coef = ws + L.coef; ga.sfin = ws + L.sfin;
+    ga.coef_ph = reinterpret_cast<const float4 *>(ws + L.coef_ph);
+    ga.coef_ab = reinterpret_cast<const float2 *>(ws + L.coef_ab);
     ga.partial = reinterpret_cast<float *>(ws + L.partial);
     ga.scratch = reinterpret_cast<float *>(ws + L.scratch);
-    ga.nslabs = (m + 31) / 32;
+    ga.nslabs = (mode & M_UNI) ? (m / 2 + 31) / 32 : (m + 31) / 32;
     switch (mode) {
         case M_FWD: k_generic<M_FWD><<<(unsigned)grid, 32, 0, st>>>(ga); break;
         case M_BUILDU: k_generic<M_BUILDU><<<(unsigned)grid, 32, 0, st>>>(ga); break;
         case M_TRANS: k_generic<M_TRANS><<<(unsigned)grid, 32, 0, st>>>(ga); break;
         case M_BWD: k_generic<M_BWD><<<(unsigned)grid, 32, 0, st>>>(ga); break;
+        case M_FWD | M_UNI: k_generic_u<M_FWD><<<(unsigned)grid, 32, 0, st>>>(ga); break;
+        case M_BUILDU | M_UNI: k_generic_u<M_BUILDU><<<(unsigned)grid, 32, 0, st>>>(ga); break;
+        case M_TRANS | M_UNI: k_generic_u<M_TRANS><<<(unsigned)grid, 32, 0, st>>>(ga); break;
+        case M_BWD | M_UNI: k_generic_u<M_BWD><<<(unsigned)grid, 32, 0, st>>>(ga); break;
+        default: return fail(GIVENS_EINVAL, "bad mode %d", mode);
     }
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -618,9 +799,74 @@ int givens_mask_from_dims(int32_t n, const uint8_t *excl, uint8_t *mask) {
 }
 
 size_t givens_workspace_bytes(int op, int32_t n, int64_t m) {
-    if (n < 2 || n > 32768 || m < 0 || op < 0 || op > 2) return 0;
-    Cfg c = make_cfg(n);
-    return ws_layout(c, op, op == GIVENS_OP_BUILD_U ? n : m).total;
+    if (n < 2 || n > 32768 || m < 0 || op < 0 || op > 5) return 0;
+    Cfg c = cfg_for_op(n, op);
+    return ws_layout(c, op, (op % 3) == GIVENS_OP_BUILD_U ? n : m).total;
+}
+
+int givens_u_supported(int32_t n) { return (n >= 2 && n <= 32768) ? 1 : 0; }
+
+int givens_u_apply(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const float *X,
+                   int64_t ldx, float *Y, int64_t ldy, int adjoint, void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_U_APPLY);
+    if (rc) return rc;
+    if (!theta || !phi || !X || !Y) return fail(GIVENS_EINVAL, "theta, phi, X and Y must be non-NULL");
+    if (ldx < m || ldy < m) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
+    if (X == Y && ldx != ldy) return fail(GIVENS_EINVAL, "in-place apply needs ldx == ldy");
+    Cfg c = make_cfg_u(n);
+    WsLayout L = ws_layout(c, GIVENS_OP_U_APPLY, m);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = (uint8_t *)ws;
+    if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi))) return rc;
+    // a complex column is two interleaved real columns
+    return run_apply_mode((adjoint ? M_TRANS : M_FWD) | M_UNI, n, 2 * m, X, 2 * ldx, nullptr, 0, Y, 2 * ldy, w, L,
+                          c, st);
+}
+
+int givens_u_build_U(int32_t n, const float *theta, const float *phi, const uint8_t *mask, float *U, int64_t ldu,
+                     void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_common(n, n, ws, ws_bytes, GIVENS_OP_U_BUILD_U);
+    if (rc) return rc;
+    if (!theta || !phi || !U) return fail(GIVENS_EINVAL, "theta, phi and U must be non-NULL");
+    if (ldu < n) return fail(GIVENS_EINVAL, "ldu < n");
+    Cfg c = make_cfg_u(n);
+    WsLayout L = ws_layout(c, GIVENS_OP_U_BUILD_U, n);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = (uint8_t *)ws;
+    if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi))) return rc;
+    return run_apply_mode(M_BUILDU | M_UNI, n, 2 * (int64_t)n, nullptr, 0, nullptr, 0, U, 2 * ldu, w, L, c, st);
+}
+
+int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
+                      const float *Y, int64_t ldy, const float *dY, int64_t lddy, float *dX, int64_t lddx,
+                      float *dtheta, float *dphi, int flags, void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_U_BACKWARD);
+    if (rc) return rc;
+    if (!theta || !phi || !Y || !dY || !dtheta || !dphi)
+        return fail(GIVENS_EINVAL, "theta, phi, Y, dY, dtheta and dphi must be non-NULL");
+    if (ldy < m || lddy < m || (dX && lddx < m)) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
+    if (dX && dX == dY && lddx != lddy) return fail(GIVENS_EINVAL, "in-place dX needs lddx == lddy");
+    Cfg c = make_cfg_u(n);
+    WsLayout L = ws_layout(c, GIVENS_OP_U_BACKWARD, m);
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *w = (uint8_t *)ws;
+    if (flags & GIVENS_FLAG_RECOMPUTE) {
+        if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi))) return rc;
+    }
+    int64_t N = givens_num_angles(n);
+    if (m == 0) {
+        CUDA_TRY(cudaMemsetAsync(dtheta, 0, (size_t)N * 4, st));
+        CUDA_TRY(cudaMemsetAsync(dphi, 0, (size_t)N * 4, st));
+        return 0;
+    }
+    if ((rc = run_apply_mode(M_BWD | M_UNI, n, 2 * m, Y, 2 * ldy, dY, 2 * lddy, dX, 2 * lddx, w, L, c, st))) return rc;
+    int64_t G = grid_for(c, M_BWD, 2 * m);
+    int64_t tot = (int64_t)2 * c.S * c.S;
+    k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, c.fast, 2, reinterpret_cast<const float *>(w + L.partial),
+        reinterpret_cast<const int32_t *>(w + L.amap), dtheta, dphi);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
 }
 
 int givens_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
@@ -676,8 +922,8 @@ int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     int64_t G = grid_for(c, M_BWD, m);
     int64_t tot = (int64_t)2 * c.S * c.S;
     k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, c.fast, reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
-        dtheta);
+        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, c.fast, 1, reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
+        dtheta, nullptr);
     CUDA_TRY(cudaGetLastError());
     return 0;
 }

@@ -41,6 +41,12 @@ __device__ __forceinline__ float cross_acc(float acc, float2 db, float2 zt, floa
     return acc + (s2.x + s2.y);
 }
 
+// dphi accumulation of the unitary backward: acc + Re(i conj(v) w) = acc + v.im w.re - v.re w.im
+__device__ __forceinline__ float phi_acc(float acc, float2 v, float2 w) {
+    return fmaf(-v.x, w.y, fmaf(v.y, w.x, acc));
+}
+__device__ __forceinline__ float phi_acc(float acc, float, float) { return acc; }
+
 __device__ __forceinline__ float shfl_up_v(float v, int w) { return __shfl_up_sync(0xffffffffu, v, 1, w); }
 __device__ __forceinline__ float2 shfl_up_v(float2 v, int w) {
     return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1, w), __shfl_up_sync(0xffffffffu, v.y, 1, w));

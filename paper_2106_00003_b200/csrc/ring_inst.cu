@@ -29,6 +29,13 @@ cudaError_t GK_CAT(ring_launch_, RING_W, RING_L)(int mode, const RingArgs &ra, i
         case M_BUILDU: return launch_wlm<RING_W, RING_L, M_BUILDU>(ra, grid, st);
         case M_TRANS: return launch_wlm<RING_W, RING_L, M_TRANS>(ra, grid, st);
         case M_BWD: return launch_wlm<RING_W, RING_L, M_BWD>(ra, grid, st);
+#if RING_W != 32 && RING_W * RING_L <= 1024  // unitary: two real columns (one complex) per thread; its
+                                                // 32-byte-per-slot tables fit shared memory up to S = 1024
+        case M_FWD | M_UNI: return launch_wlm<RING_W, RING_L, M_FWD | M_UNI>(ra, grid, st);
+        case M_BUILDU | M_UNI: return launch_wlm<RING_W, RING_L, M_BUILDU | M_UNI>(ra, grid, st);
+        case M_TRANS | M_UNI: return launch_wlm<RING_W, RING_L, M_TRANS | M_UNI>(ra, grid, st);
+        case M_BWD | M_UNI: return launch_wlm<RING_W, RING_L, M_BWD | M_UNI>(ra, grid, st);
+#endif
     }
     return cudaErrorInvalidValue;
 }

@@ -11,7 +11,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import FLAG_RECOMPUTE, OP_APPLY, OP_BACKWARD, OP_BUILD_U, check, lib
+from ._lib import (FLAG_RECOMPUTE, OP_APPLY, OP_BACKWARD, OP_BUILD_U, OP_U_APPLY, OP_U_BACKWARD, OP_U_BUILD_U,
+                   check, lib)
 
 
 def num_angles(n: int) -> int:
@@ -229,3 +230,70 @@ class HostPipeline:
         self.dth_host.copy_(self.dth, non_blocking=True)
         self.n_done += 1
         return self.dth_host
+
+
+# ---------------------------------------------------------------- unitary U(n) (Appendix A)
+
+def u_supported(n: int) -> bool:
+    return bool(lib().givens_u_supported(n))
+
+
+def _check_cmatrix(name, t, n):
+    if not (t.is_cuda and t.dtype == torch.complex64 and t.dim() == 2 and t.shape[0] == n and t.stride(1) == 1):
+        raise ValueError(f"{name} must be a CUDA complex64 [n, m] tensor with unit column stride "
+                         f"(got {tuple(t.shape)} {t.dtype} {t.device} strides {t.stride()})")
+
+
+def _check_phi(phi, n):
+    N = num_angles(n)
+    if not (phi.is_cuda and phi.dtype == torch.float32 and phi.is_contiguous() and phi.numel() == N):
+        raise ValueError(f"phi must be a contiguous CUDA float32 tensor of {N} phase angles")
+
+
+def u_apply(theta, phi, X, mask=None, adjoint: bool = False, out=None, ws=None):
+    """Y = U(theta, phi) X or U^dagger X (Algorithm 4), X complex64 [n, m]."""
+    n, m = X.shape
+    _check_cmatrix("X", X, n)
+    _check_theta(theta, mask, n)
+    _check_phi(phi, n)
+    Y = torch.empty_like(X) if out is None else out
+    _check_cmatrix("out", Y, n)
+    if ws is None:
+        ws = workspace(OP_U_APPLY, n, m, X.device)
+    check(lib().givens_u_apply(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y),
+                               Y.stride(0), int(bool(adjoint)), _ptr(ws), ws.numel(), _stream(X.device)))
+    return Y
+
+
+def u_build_U(theta, phi, n: int, mask=None, out=None, ws=None):
+    """U = U(theta, phi) in U(n), complex64 [n, n]."""
+    _check_theta(theta, mask, n)
+    _check_phi(phi, n)
+    U = torch.empty((n, n), dtype=torch.complex64, device=theta.device) if out is None else out
+    _check_cmatrix("U", U, n)
+    if ws is None:
+        ws = workspace(OP_U_BUILD_U, n, n, theta.device)
+    check(lib().givens_u_build_U(n, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(U), U.stride(0), _ptr(ws), ws.numel(),
+                                 _stream(theta.device)))
+    return U
+
+
+def u_backward(theta, phi, Y, dY, mask=None, want_dX: bool = True, ws=None, recompute: bool = True):
+    """(dtheta, dphi, dX) for a real loss of Y = U X, dY = dL/dRe(Y) + i dL/dIm(Y)."""
+    n, m = Y.shape
+    _check_cmatrix("Y", Y, n)
+    _check_cmatrix("dY", dY, n)
+    _check_theta(theta, mask, n)
+    _check_phi(phi, n)
+    if ws is None:
+        ws = workspace(OP_U_BACKWARD, n, m, Y.device)
+        recompute = True
+    N = num_angles(n)
+    dtheta = torch.empty(N, dtype=torch.float32, device=Y.device)
+    dphi = torch.empty(N, dtype=torch.float32, device=Y.device)
+    dX = torch.empty_like(dY) if want_dX else None
+    check(lib().givens_u_backward(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY),
+                                  dY.stride(0), _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
+                                  _ptr(dphi), FLAG_RECOMPUTE if recompute else 0, _ptr(ws), ws.numel(),
+                                  _stream(Y.device)))
+    return dtheta, dphi, dX
