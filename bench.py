@@ -204,6 +204,50 @@ def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 409
     return table
 
 
+# flops per complex rotation-column of the unitary kernels: two real three-shear rotations
+# (2 x 6) + the phase multiply (6); backward: Z and D replay (2 x 18) + dtheta (8) + dphi (20)
+UFLOPS_FWD, UFLOPS_BWD = 18, 64
+
+
+def unitary_line(g, torch, synth, dev, peak_tflops, n=1024, m=32768, reps=5):
+    """the unitary U(n) path (Appendix A) at n = 1024 on m complex columns (the same
+    2m = 65536 real columns as C3): device ms of u_apply and u_backward, mean of `reps` after
+    warm-up, L2 flushed before each."""
+    N = n * (n - 1) // 2
+    th = torch.from_numpy(synth.theta(N, seed=SEED)).to(dev)
+    ph = torch.from_numpy(synth.theta(N, seed=SEED + 1)).to(dev)
+    X = torch.complex(torch.from_numpy(synth.normal_matrix(n, m, SEED, synth.TID_X)),
+                      torch.from_numpy(synth.normal_matrix(n, m, SEED + 1, synth.TID_X))).to(dev)
+    G = torch.complex(torch.from_numpy(synth.normal_matrix(n, m, SEED, synth.TID_DY)),
+                      torch.from_numpy(synth.normal_matrix(n, m, SEED + 1, synth.TID_DY))).to(dev)
+    wsb = g.workspace(g.OP_U_BACKWARD, n, m, dev)
+    wsf = g.workspace(g.OP_U_APPLY, n, m, dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    Y = g.u_apply(th, ph, X, ws=wsf)
+    g.u_backward(th, ph, Y, G, ws=wsb)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    tf = tb = 0.0
+    for _ in range(reps):
+        flush.fill_(1.0)
+        ev[0].record()
+        g.u_apply(th, ph, X, out=Y, ws=wsf)
+        ev[1].record()
+        flush.fill_(2.0)
+        ev[2].record()
+        g.u_backward(th, ph, Y, G, ws=wsb)
+        ev[3].record()
+        torch.cuda.synchronize()
+        tf += ev[0].elapsed_time(ev[1])
+        tb += ev[2].elapsed_time(ev[3])
+    tf, tb = tf / reps, tb / reps
+    return {"workload": f"unitary n={n}, m={m} complex columns (fp32 re/im), u_apply + u_backward (dtheta, dphi, dX)",
+            "fwd_ms": round(tf, 4), "bwd_ms": round(tb, 4),
+            "complex_rotations_per_s": N * m / ((tf + tb) * 1e-3),
+            "fwd_frac": UFLOPS_FWD * N * m / (tf * 1e-3) / 1e12 / peak_tflops,
+            "bwd_frac": UFLOPS_BWD * N * m / (tb * 1e-3) / 1e12 / peak_tflops,
+            "flops_per_complex_rotation_column": {"fwd": UFLOPS_FWD, "bwd": UFLOPS_BWD}}
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -365,6 +409,8 @@ def main():
             out["e2e"] = e2e
         if ubuild:
             out["ubuild_ms_vs_n"] = ubuild
+        if world == 1 and not args.no_ubuild:
+            out["unitary"] = unitary_line(g, torch, synth, dev, peak)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out), flush=True)

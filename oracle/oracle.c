@@ -25,6 +25,14 @@
  *
  * Pins: see tests/test_oracle_pins.py (paper Eq. (5), SPEC n=4 example, paper §5 n=8/m=4
  * list, closed forms, invariants, dense explicit products, finite differences).
+ *
+ * Layout options: every schedule-consuming function takes
+ *   perm  -- the circle method's initial sequence ("Beginning with an arbitrary
+ *            permutation of the coordinate sequence"), a permutation of
+ *            0..n_eff-1 (odd n: it includes the bye index n); NULL = identity (Fig. 1);
+ *   refl  -- reflection (det -1) by "negating an arbitrary fixed column following the
+ *            construction": U' = U with column refl negated; -1 = none.
+ *            Y = U' X = U (D X) with D = diag(.., -1 at refl, ..); U'^T X = D (U^T X).
  */
 #include <math.h>
 #include <stdint.h>
@@ -58,13 +66,23 @@ int64_t oracle_num_angles(int n) { return n < 2 ? -1 : (int64_t)n * (n - 1) / 2;
  * of the angle in theta (block-major: b_1 first, pairs in listed order), or -1.
  * Either output may be NULL. Returns the number of real pairs (n(n-1)/2), or -1.
  */
-int64_t oracle_schedule(int n, int32_t *pairs, int64_t *flat) {
+int64_t oracle_schedule(int n, const int32_t *perm, int32_t *pairs, int64_t *flat) {
     if (n < 2) return -1;
     int ne = n_eff_of(n);
     int R = ne - 1, S = ne / 2;
+    if (perm) { /* must be a permutation of 0..ne-1 */
+        char *seen = (char *)calloc(ne, 1);
+        int ok = 1;
+        for (int p = 0; p < ne; p++) {
+            if (perm[p] < 0 || perm[p] >= ne || seen[perm[p]]) ok = 0;
+            else seen[perm[p]] = 1;
+        }
+        free(seen);
+        if (!ok) return -1;
+    }
     int *seq = (int *)malloc(sizeof(int) * ne);
     int *nxt = (int *)malloc(sizeof(int) * ne);
-    for (int p = 0; p < ne; p++) seq[p] = p;
+    for (int p = 0; p < ne; p++) seq[p] = perm ? perm[p] : p;
     int64_t f = 0;
     for (int r = 0; r < R; r++) {
         for (int k = 0; k < S; k++) {
@@ -85,12 +103,13 @@ int64_t oracle_schedule(int n, int32_t *pairs, int64_t *flat) {
 }
 
 /* The sequence E as a flat list of the real pairs in angle order. */
-static int32_t *build_E(int n, int64_t *N_out) {
+static int32_t *build_E(int n, const int32_t *perm, int64_t *N_out) {
     int ne = n_eff_of(n);
     int R = ne - 1, S = ne / 2;
     int32_t *pairs = (int32_t *)malloc(sizeof(int32_t) * 2 * (size_t)R * S);
     int64_t *flat = (int64_t *)malloc(sizeof(int64_t) * (size_t)R * S);
-    int64_t N = oracle_schedule(n, pairs, flat);
+    int64_t N = oracle_schedule(n, perm, pairs, flat);
+    if (N < 0) { free(pairs); free(flat); return NULL; }
     int32_t *E = (int32_t *)malloc(sizeof(int32_t) * 2 * (size_t)N);
     for (int64_t q = 0; q < (int64_t)R * S; q++) {
         if (flat[q] < 0) continue;
@@ -133,12 +152,14 @@ int oracle_apply_sequence(int n, int64_t m, int64_t Np, const int32_t *E, const 
 /*
  * Y = U(theta) X (transpose=0) or U^T X (transpose=1) with E the circle-method round-robin
  * sequence. Columns are split into fixed blocks; each block runs Algorithm 1 on its columns.
+ * Reflection: the block's row refl is negated before Algorithm 1 (transpose: after).
  */
-int oracle_apply(int n, int64_t m, const float *theta, const uint8_t *mask, const double *X,
-                 double *Y, int transpose) {
-    if (n < 2 || m < 0) return -1;
+int oracle_apply(int n, int64_t m, const int32_t *perm, int refl, const float *theta, const uint8_t *mask,
+                 const double *X, double *Y, int transpose) {
+    if (n < 2 || m < 0 || refl < -1 || refl >= n) return -1;
     int64_t N;
-    int32_t *E = build_E(n, &N);
+    int32_t *E = build_E(n, perm, &N);
+    if (!E) return -1;
     const int64_t CB = 64;
     int64_t nb = (m + CB - 1) / CB;
     int rc = 0;
@@ -148,7 +169,11 @@ int oracle_apply(int n, int64_t m, const float *theta, const uint8_t *mask, cons
         double *blk = (double *)malloc(sizeof(double) * (size_t)n * w);
         for (int r = 0; r < n; r++)
             for (int64_t l = 0; l < w; l++) blk[(int64_t)r * w + l] = X[(int64_t)r * m + c0 + l];
+        if (refl >= 0 && !transpose)
+            for (int64_t l = 0; l < w; l++) blk[(int64_t)refl * w + l] = -blk[(int64_t)refl * w + l];
         if (oracle_apply_sequence(n, w, N, E, theta, mask, blk, w, transpose)) rc = -1;
+        if (refl >= 0 && transpose)
+            for (int64_t l = 0; l < w; l++) blk[(int64_t)refl * w + l] = -blk[(int64_t)refl * w + l];
         for (int r = 0; r < n; r++)
             for (int64_t l = 0; l < w; l++) Y[(int64_t)r * m + c0 + l] = blk[(int64_t)r * w + l];
         free(blk);
@@ -158,11 +183,11 @@ int oracle_apply(int n, int64_t m, const float *theta, const uint8_t *mask, cons
 }
 
 /* U = U(theta): Algorithm 1 / 2 starting from U <- I_n. */
-int oracle_build_U(int n, const float *theta, const uint8_t *mask, double *U) {
+int oracle_build_U(int n, const int32_t *perm, int refl, const float *theta, const uint8_t *mask, double *U) {
     if (n < 2) return -1;
     double *I = (double *)calloc((size_t)n * n, sizeof(double));
     for (int r = 0; r < n; r++) I[(int64_t)r * n + r] = 1.0;
-    int rc = oracle_apply(n, n, theta, mask, I, U, 0);
+    int rc = oracle_apply(n, n, perm, refl, theta, mask, I, U, 0);
     free(I);
     return rc;
 }
@@ -178,13 +203,14 @@ int oracle_build_U(int n, const float *theta, const uint8_t *mask, double *U) {
  * Masked angles are not parameters: their dtheta is exactly 0.
  * dtheta is summed in fp64 over columns in increasing column order within each thread's
  * fixed contiguous column range; thread partials are combined in thread order.
- * dX may be NULL.
+ * dX may be NULL. Reflection: the forward starts from D X and dX = D (gradient w.r.t. D X).
  */
-int oracle_backward(int n, int64_t m, const float *theta, const uint8_t *mask, const double *X,
-                    const double *dY, double *dX, double *dtheta) {
-    if (n < 2 || m < 0) return -1;
+int oracle_backward(int n, int64_t m, const int32_t *perm, int refl, const float *theta, const uint8_t *mask,
+                    const double *X, const double *dY, double *dX, double *dtheta) {
+    if (n < 2 || m < 0 || refl < -1 || refl >= n) return -1;
     int64_t N;
-    int32_t *E = build_E(n, &N);
+    int32_t *E = build_E(n, perm, &N);
+    if (!E) return -1;
     double *cs = (double *)malloc(sizeof(double) * 2 * (size_t)N);
     for (int64_t e = 0; e < N; e++) {
         double th = (double)theta[e];
@@ -206,6 +232,7 @@ int oracle_backward(int n, int64_t m, const float *theta, const uint8_t *mask, c
         double *tape = (double *)malloc(sizeof(double) * 2 * (size_t)N);
         for (int64_t col = c0; col < c1; col++) {
             for (int r = 0; r < n; r++) x[r] = X[(int64_t)r * m + col];
+            if (refl >= 0) x[refl] = -x[refl];
             /* forward, Algorithm 1 order: e = e_N, ..., e_1 */
             for (int64_t e = N - 1; e >= 0; e--) {
                 if (mask && !mask[e]) continue;
@@ -229,6 +256,7 @@ int oracle_backward(int n, int64_t m, const float *theta, const uint8_t *mask, c
                 g[i] = c * gi + s * gj;
                 g[j] = -s * gi + c * gj;
             }
+            if (refl >= 0) g[refl] = -g[refl];
             if (dX)
                 for (int r = 0; r < n; r++) dX[(int64_t)r * m + col] = g[r];
         }
@@ -254,14 +282,15 @@ int oracle_backward(int n, int64_t m, const float *theta, const uint8_t *mask, c
  *     d <- A 1;  dL/dtheta_e <- d_{m(e)}
  * m(e) = slot index of e in its block. Bye (j == n) and masked pairs are bypassed.
  */
-int oracle_alg3(int n, const float *theta, const uint8_t *mask, const double *U,
+int oracle_alg3(int n, const int32_t *perm, const float *theta, const uint8_t *mask, const double *U,
                 const double *Gamma, double *dtheta) {
     if (n < 2) return -1;
     int ne = n_eff_of(n);
     int R = ne - 1, S = ne / 2;
     int32_t *pairs = (int32_t *)malloc(sizeof(int32_t) * 2 * (size_t)R * S);
     int64_t *flat = (int64_t *)malloc(sizeof(int64_t) * (size_t)R * S);
-    int64_t N = oracle_schedule(n, pairs, flat);
+    int64_t N = oracle_schedule(n, perm, pairs, flat);
+    if (N < 0) { free(pairs); free(flat); return -1; }
     double *Uf = (double *)malloc(sizeof(double) * (size_t)n * n);
     double *M = (double *)malloc(sizeof(double) * (size_t)n * n);
     double *A = (double *)malloc(sizeof(double) * (size_t)S * n);
@@ -327,14 +356,17 @@ int oracle_alg3(int n, const float *theta, const uint8_t *mask, const double *U,
  * for e in reversed(E): r_i <- e^{i phi} cos U_i - sin U_j ; r_j <- e^{i phi} sin U_i + cos U_j.
  * adjoint = 1 applies U^dagger = G^{e_N dagger} ... G^{e_1 dagger}: e in E order with
  * G^dagger = [[e^{-i phi} c, e^{-i phi} s], [-s, c]]. */
-int oracle_u_apply(int n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const double *X,
-                   double *Y, int adjoint) {
-    if (n < 2 || m < 0) return -1;
+int oracle_u_apply(int n, int64_t m, const int32_t *perm, int refl, const float *theta, const float *phi,
+                   const uint8_t *mask, const double *X, double *Y, int adjoint) {
+    if (n < 2 || m < 0 || refl < -1 || refl >= n) return -1;
     int64_t N;
-    int32_t *E = build_E(n, &N);
+    int32_t *E = build_E(n, perm, &N);
+    if (!E) return -1;
     memcpy(Y, X, sizeof(double) * 2 * (size_t)n * m);
 #pragma omp parallel for schedule(static)
     for (int64_t col = 0; col < m; col++) {
+        double *yc = Y + ((int64_t)(refl >= 0 ? refl : 0) * m + col) * 2;
+        if (refl >= 0 && !adjoint) { yc[0] = -yc[0]; yc[1] = -yc[1]; }
         for (int64_t q = 0; q < N; q++) {
             int64_t e = adjoint ? q : (N - 1 - q);
             if (mask && !mask[e]) continue;
@@ -357,6 +389,7 @@ int oracle_u_apply(int n, int64_t m, const float *theta, const float *phi, const
                 yj[1] = -s * ai + c * bi;
             }
         }
+        if (refl >= 0 && adjoint) { yc[0] = -yc[0]; yc[1] = -yc[1]; }
     }
     free(E);
     return 0;
@@ -369,11 +402,13 @@ int oracle_u_apply(int n, int64_t m, const float *theta, const float *phi, const
  *   dy_i/dtheta = -e^{i phi} s a_i - c a_j,  dy_j/dtheta = e^{i phi} c a_i - s a_j,
  *   dy_i/dphi = i e^{i phi} c a_i,           dy_j/dphi = i e^{i phi} s a_i,
  *   g_a_i = conj(e^{i phi}) (c g_i + s g_j),  g_a_j = -s g_i + c g_j   (adjoint of the 2x2 map). */
-int oracle_u_backward(int n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const double *X,
-                      const double *G, double *dX, double *dtheta, double *dphi) {
-    if (n < 2 || m < 0) return -1;
+int oracle_u_backward(int n, int64_t m, const int32_t *perm, int refl, const float *theta, const float *phi,
+                      const uint8_t *mask, const double *X, const double *G, double *dX, double *dtheta,
+                      double *dphi) {
+    if (n < 2 || m < 0 || refl < -1 || refl >= n) return -1;
     int64_t N;
-    int32_t *E = build_E(n, &N);
+    int32_t *E = build_E(n, perm, &N);
+    if (!E) return -1;
     int nt = oracle_num_threads();
     double *pt = (double *)calloc((size_t)nt * N, sizeof(double));
     double *pp = (double *)calloc((size_t)nt * N, sizeof(double));
@@ -393,6 +428,7 @@ int oracle_u_backward(int n, int64_t m, const float *theta, const float *phi, co
                 x[2 * r] = X[((int64_t)r * m + col) * 2];
                 x[2 * r + 1] = X[((int64_t)r * m + col) * 2 + 1];
             }
+            if (refl >= 0) { x[2 * refl] = -x[2 * refl]; x[2 * refl + 1] = -x[2 * refl + 1]; }
             for (int64_t e = N - 1; e >= 0; e--) {
                 if (mask && !mask[e]) continue;
                 int i = E[2 * e], j = E[2 * e + 1];
@@ -433,6 +469,7 @@ int oracle_u_backward(int n, int64_t m, const float *theta, const float *phi, co
                 g[2 * j] = -s * gir + c * gjr;
                 g[2 * j + 1] = -s * gii + c * gji;
             }
+            if (refl >= 0) { g[2 * refl] = -g[2 * refl]; g[2 * refl + 1] = -g[2 * refl + 1]; }
             if (dX)
                 for (int r = 0; r < n; r++) {
                     dX[((int64_t)r * m + col) * 2] = g[2 * r];
