@@ -156,6 +156,54 @@ int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi
                       const float *Y, int64_t ldy, const float *dY, int64_t lddy, float *dX, int64_t lddx,
                       float *dtheta, float *dphi, int flags, void *ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------------------------------
+ * Layout options.
+ * perm         the circle method's initial sequence ("Beginning with an
+ *              arbitrary permutation of the coordinate sequence"): a
+ *              permutation of 0..n_eff-1 (odd n: it contains the bye index n), NULL = identity
+ *              (Fig. 1). Block b_{r+1} then pairs perm[s_r[k]] with perm[s_r[n_eff-1-k]]; theta
+ *              stays in block-major flat order over the resulting pairs (byes skipped). In the
+ *              _ex compute calls perm is a DEVICE pointer (int32[n_eff]) and must be valid --
+ *              check it on the host with givens_check_perm (the kernels do not). In
+ *              givens_schedule_ex / givens_mask_from_dims_ex it is a HOST pointer and is checked.
+ * reflect_col  -1, or a column c in [0, n): the reflection class (det -1) "by ... negating an
+ *              arbitrary fixed column following the construction":
+ *              U' = U diag(.., -1 at c, ..). apply: Y = U' X; transpose: U'^T X; backward:
+ *              dtheta of L(U' X), dX = U'^T dY. Costs nothing in the kernels (it is one more
+ *              sign in the per-row sign bookkeeping).
+ * A givens_backward_ex without GIVENS_FLAG_RECOMPUTE must use the workspace of a forward call
+ * with the same (n, theta, mask, perm, reflect_col). The calls without _ex are the _ex calls
+ * with perm = NULL, reflect_col = -1.
+ * ------------------------------------------------------------------------------------------ */
+
+/* 0 if perm_host (int32[n_eff], host) is a permutation of 0..n_eff-1 (NULL counts as valid),
+ * else GIVENS_EINVAL with the offending entry in givens_last_error(). */
+int givens_check_perm(int32_t n, const int32_t *perm_host);
+
+/* givens_schedule / givens_mask_from_dims for the start sequence perm_host (host, checked). */
+int givens_schedule_ex(int32_t n, const int32_t *perm_host, int32_t *pairs_host, int64_t *flat_host);
+int givens_mask_from_dims_ex(int32_t n, const int32_t *perm_host, const uint8_t *excluded_dims_host,
+                             uint8_t *mask_host);
+
+int givens_apply_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
+                    float *Y, int64_t ldy, int transpose, const int32_t *perm, int32_t reflect_col, void *ws,
+                    size_t ws_bytes, void *stream);
+int givens_build_U_ex(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu,
+                      const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes, void *stream);
+int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *Y, int64_t ldy,
+                       const float *dY, int64_t lddy, float *dX, int64_t lddx, float *dtheta, int flags,
+                       const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes, void *stream);
+int givens_u_apply_ex(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
+                      const float *X, int64_t ldx, float *Y, int64_t ldy, int adjoint, const int32_t *perm,
+                      int32_t reflect_col, void *ws, size_t ws_bytes, void *stream);
+int givens_u_build_U_ex(int32_t n, const float *theta, const float *phi, const uint8_t *mask, float *U,
+                        int64_t ldu, const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes,
+                        void *stream);
+int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
+                         const float *Y, int64_t ldy, const float *dY, int64_t lddy, float *dX, int64_t lddx,
+                         float *dtheta, float *dphi, int flags, const int32_t *perm, int32_t reflect_col,
+                         void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

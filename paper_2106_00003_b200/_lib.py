@@ -20,7 +20,9 @@ EXPORTS = [
     "givens_last_error", "givens_version", "givens_num_angles", "givens_supported",
     "givens_schedule", "givens_mask_from_dims", "givens_workspace_bytes", "givens_apply",
     "givens_build_U", "givens_backward", "givens_index_trace", "givens_u_supported", "givens_u_apply",
-    "givens_u_build_U", "givens_u_backward",
+    "givens_u_build_U", "givens_u_backward", "givens_check_perm", "givens_schedule_ex", "givens_mask_from_dims_ex",
+    "givens_apply_ex", "givens_build_U_ex", "givens_backward_ex", "givens_u_apply_ex", "givens_u_build_U_ex",
+    "givens_u_backward_ex",
 ]
 
 
@@ -70,6 +72,24 @@ def lib():
         L.givens_u_build_U.argtypes = [I32, P, P, P, P, I64, P, SZ, P]
         L.givens_u_backward.restype = C
         L.givens_u_backward.argtypes = [I32, I64, P, P, P, P, I64, P, I64, P, I64, P, P, C, P, SZ, P]
+        L.givens_check_perm.restype = C
+        L.givens_check_perm.argtypes = [I32, P]
+        L.givens_schedule_ex.restype = C
+        L.givens_schedule_ex.argtypes = [I32, P, P, P]
+        L.givens_mask_from_dims_ex.restype = C
+        L.givens_mask_from_dims_ex.argtypes = [I32, P, P, P]
+        L.givens_apply_ex.restype = C
+        L.givens_apply_ex.argtypes = [I32, I64, P, P, P, I64, P, I64, C, P, I32, P, SZ, P]
+        L.givens_build_U_ex.restype = C
+        L.givens_build_U_ex.argtypes = [I32, P, P, P, I64, P, I32, P, SZ, P]
+        L.givens_backward_ex.restype = C
+        L.givens_backward_ex.argtypes = [I32, I64, P, P, P, I64, P, I64, P, I64, P, C, P, I32, P, SZ, P]
+        L.givens_u_apply_ex.restype = C
+        L.givens_u_apply_ex.argtypes = [I32, I64, P, P, P, P, I64, P, I64, C, P, I32, P, SZ, P]
+        L.givens_u_build_U_ex.restype = C
+        L.givens_u_build_U_ex.argtypes = [I32, P, P, P, P, I64, P, I32, P, SZ, P]
+        L.givens_u_backward_ex.restype = C
+        L.givens_u_backward_ex.argtypes = [I32, I64, P, P, P, P, I64, P, I64, P, I64, P, P, C, P, I32, P, SZ, P]
         _lib = L
     return _lib
 

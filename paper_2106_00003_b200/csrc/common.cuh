@@ -35,12 +35,25 @@ __host__ __device__ inline int64_t flat_of(int r, int k, int n, int ne) {
     if (k == kb) return -1;
     return (int64_t)r * (S - 1) + k - (k > kb ? 1 : 0);
 }
-// position of row i in s_r
+// position of label i in s_r
 __host__ __device__ inline int pos_of(int i, int r, int ne) {
     if (i == 0) return 0;
     int R = ne - 1;
     return 1 + ((i - 1 + r) % R);
 }
+// Start permutation: the ring works on labels 0..n_eff-1 (the
+// positions of the identity start sequence); label l is row perm[l]. Odd n: the bye is the label
+// bl with perm[bl] = n. flat index of (block r, slot k) with the bye at label bl.
+__host__ __device__ inline int64_t flat_of_bl(int r, int k, int n, int ne, int bl) {
+    int S = ne / 2;
+    if (n == ne) return (int64_t)r * S + k;
+    int p = pos_of(bl, r, ne);
+    int kb = p < ne - 1 - p ? p : ne - 1 - p;
+    if (k == kb) return -1;
+    return (int64_t)r * (S - 1) + k - (k > kb ? 1 : 0);
+}
+// workspace layout block (k_layout): lay[0..ne) = row of each label, lay[ne] = bye label (odd n),
+// lay[ne + 1] = label of the reflected column (-1: none)
 
 #ifndef GK_BWD_WARPS
 #define GK_BWD_WARPS 8
@@ -120,7 +133,8 @@ struct RingArgs {
     const uint8_t *coef;     // (t, s) per slot, lane-chunked rows
     const uint8_t *coef_ph;  // unitary: (p_t, q_t, p_b, q_b) phase factors per slot
     const uint8_t *coef_ab;  // unitary backward: (alpha, beta) dphi weights per slot
-    const uint8_t *sfin;
+    const uint8_t *sfin;     // final sign per label
+    const int32_t *lrow;     // row of each label (start permutation; >= n for the odd-n bye)
     float *partial;   // BWD: per CTA, per reduction group, NW warp blocks (see red_geom)
     int64_t nslabs;
     int vec_ok;       // 1 if all row starts are 16-byte aligned for K-wide vector access
@@ -478,10 +492,11 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         for (int q = 0; q < W; q++) {
             const int k = t * W + q;
             const int pt = k, pb = ne - 1 - k;
-            int rt, rb;
-            if (UP) { rt = row_sRm1(pt, ne); rb = row_sRm1(pb, ne); }
-            else    { rt = row_s0(pt);       rb = row_s0(pb); }
-            if (!active) rt = rb = n;  // idle lanes hold zeros and never store
+            int lt, lb;  // labels
+            if (UP) { lt = row_sRm1(pt, ne); lb = row_sRm1(pb, ne); }
+            else    { lt = row_s0(pt);       lb = row_s0(pb); }
+            int rt = n, rb = n;  // rows; idle lanes hold zeros and never store
+            if (active) { rt = a.lrow[lt]; rb = a.lrow[lb]; }
             V vt[KP], vb[KP];
             if constexpr (BM == M_BUILDU && UNI) {
 #pragma unroll
@@ -504,7 +519,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
             }
             if (UP) {
-                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+                const bool nt = rt < n && a.sfin[lt], nb = rb < n && a.sfin[lb];
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }
@@ -515,7 +530,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else for (int p = 0; p < KP; p++) vt[p] = V{};
                 if (rb < n) IO::load(a.dY + (int64_t)rb * a.lddy, col0, a.m, a.vec_ok, vb);
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
-                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+                const bool nt = rt < n && a.sfin[lt], nb = rb < n && a.sfin[lb];
 #pragma unroll
                 for (int p = 0; p < KP; p++) {
                     DT[p][q] = vneg_if(vt[p], nt);
@@ -568,7 +583,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                             // dz_bottom * z_top - dz_top * z_bottom (Q_e structure, PAPER.md:515-521;
                             // in the unitary variant Re(conj(dz_b) z_t - conj(dz_t) z_b), the same
                             // sum over the (re, im) halves)
-                            float c = cross_acc(0.f, DB[0][q], ZT[0][q], DT[0][q], ZB[0][q]);
+                            float c = cross_first(DB[0][q], ZT[0][q], DT[0][q], ZB[0][q]);
 #pragma unroll
                             for (int p = 1; p < KP; p++) c = cross_acc(c, DB[p][q], ZT[p][q], DT[p][q], ZB[p][q]);
                             acc[LC > 1 ? q : (q & 3)] = c;
@@ -746,10 +761,11 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         for (int q = 0; q < W; q++) {
             const int k = t * W + q;
             const int pt = k, pb = ne - 1 - k;
-            int rt, rb;
-            if (UP) { rt = row_s0(pt); rb = row_s0(pb); }
-            else    { rt = row_sRm1(pt, ne); rb = row_sRm1(pb, ne); }
-            if (!active) rt = rb = n;
+            int lt, lb;
+            if (UP) { lt = row_s0(pt); lb = row_s0(pb); }
+            else    { lt = row_sRm1(pt, ne); lb = row_sRm1(pb, ne); }
+            int rt = n, rb = n;
+            if (active) { rt = a.lrow[lt]; rb = a.lrow[lb]; }
             V vt[KP], vb[KP];
 #pragma unroll
             for (int p = 0; p < KP; p++) {
@@ -757,7 +773,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else { vt[p] = ZT[p][q]; vb[p] = ZB[p][q]; }
             }
             if (!UP) {
-                const bool nt = rt < n && a.sfin[rt], nb = rb < n && a.sfin[rb];
+                const bool nt = rt < n && a.sfin[lt], nb = rb < n && a.sfin[lb];
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }

@@ -158,7 +158,7 @@ int64_t grid_for(const Cfg &c, int mode, int64_t m) {
 }
 
 struct WsLayout {
-    size_t coef, coef_ph, coef_ab, amap, flip, sig, sfin, partial, scratch, total;
+    size_t coef, coef_ph, coef_ab, amap, flip, sig, sfin, lay, partial, scratch, total;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
@@ -178,6 +178,7 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     L.flip = off; off = al256(off + (size_t)c.R * c.S);
     L.sig = off; off = al256(off + (size_t)c.R * c.ne);
     L.sfin = off; off = al256(off + (size_t)c.ne);
+    L.lay = off; off = al256(off + (size_t)(c.ne + 2) * 4);
     L.partial = off;
     if (base == GIVENS_OP_BACKWARD) {
         int64_t g = grid_for(c, M_BWD, mr);
@@ -203,14 +204,30 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
 namespace gk {
 
 // ------------------------------------------------------------------ precompute kernels
+// (0) layout block (one CTA): row of each label under the start permutation perm (NULL =
+// identity), the odd-n bye label, and the label of the reflected column.
+__global__ void k_layout(int n, int ne, const int32_t *__restrict__ perm, int refl, int32_t *__restrict__ lay) {
+    if (threadIdx.x == 0) {
+        lay[ne] = ne - 1;  // identity: the bye is label n
+        lay[ne + 1] = refl;
+    }
+    __syncthreads();
+    for (int l = threadIdx.x; l < ne; l += blockDim.x) {
+        int row = perm ? perm[l] : l;
+        lay[l] = row;
+        if (perm && row == n && n != ne) lay[ne] = l;
+        if (perm && refl >= 0 && row == refl) lay[ne + 1] = l;
+    }
+}
+
 // (1) flip bit per (block, slot): |theta| > pi/2 => R(theta) = -R(theta -/+ pi).
 __global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uint8_t *__restrict__ mask,
-                       uint8_t *__restrict__ flip) {
+                       const int32_t *__restrict__ lay, uint8_t *__restrict__ flip) {
     int S = ne / 2, R = ne - 1;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)R * S) return;
     int r = (int)(idx / S), k = (int)(idx % S);
-    int64_t f = flat_of(r, k, n, ne);
+    int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
     uint8_t fl = 0;
     if (f >= 0 && (!mask || mask[f])) fl = fabs((double)theta[f]) > 1.5707963267948966 ? 1 : 0;
     flip[idx] = fl;
@@ -220,8 +237,10 @@ __global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uin
 // (forward applies b_R first), i.e. blocks r' > r. sig[r][row], sfin[row].
 // One warp per row: lane l owns a contiguous segment of blocks (highest blocks in lane 0); an
 // exclusive prefix XOR over the lanes gives each segment its starting parity.
-__global__ void k_sigma(int ne, const uint8_t *__restrict__ flip, uint8_t *__restrict__ sig,
-                        uint8_t *__restrict__ sfin) {
+// A reflection D (applied before every block) flips the parity of its label in every block and
+// in sfin; the kernels then load and store without knowing about it.
+__global__ void k_sigma(int ne, const uint8_t *__restrict__ flip, const int32_t *__restrict__ lay,
+                        uint8_t *__restrict__ sig, uint8_t *__restrict__ sfin) {
     const int S = ne / 2, R = ne - 1;
     const int lane = threadIdx.x & 31;
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -243,12 +262,13 @@ __global__ void k_sigma(int ne, const uint8_t *__restrict__ flip, uint8_t *__res
         uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl ^= v;
     }
-    uint32_t par = incl ^ x;
+    const uint32_t rf = (lay[ne + 1] == i) ? 1u : 0u;
+    uint32_t par = incl ^ x ^ rf;
     for (int r = hi; r >= lo; r--) {
         sig[(int64_t)r * ne + i] = (uint8_t)par;
         par ^= flip_at(r);
     }
-    if (lane == 31) sfin[i] = (uint8_t)incl;
+    if (lane == 31) sfin[i] = (uint8_t)(incl ^ rf);
 }
 
 __device__ __forceinline__ int coef_pos(int k, int W, int L) {
@@ -263,7 +283,8 @@ __device__ __forceinline__ int coef_pos(int k, int W, int L) {
 // orientation (top row < bottom row); amap[rho][k] = flat | neg<<30 | masked<<29, or -1.
 __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *__restrict__ theta,
                        const uint8_t *__restrict__ mask, const uint8_t *__restrict__ flip,
-                       const uint8_t *__restrict__ sig, uint8_t *__restrict__ coef, int32_t *__restrict__ amap) {
+                       const uint8_t *__restrict__ sig, const int32_t *__restrict__ lay, uint8_t *__restrict__ coef,
+                       int32_t *__restrict__ amap) {
     int S = ne / 2, R = ne - 1;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)(R + 2) * S) return;
@@ -276,13 +297,13 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
         return;
     }
     int r = rho - 1;
-    int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);
-    int64_t f = flat_of(r, k, n, ne);
+    int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);  // labels; rows lay[a], lay[b]
+    int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
     bool active = f >= 0 && (!mask || mask[f]);
     double th = active ? (double)theta[f] : 0.0;
     double phi = th;
     if (fabs(th) > 1.5707963267948966) phi = th - copysign(3.141592653589793, th);
-    int neg = (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) ^ (a > b ? 1 : 0);
+    int neg = (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) ^ (lay[a] > lay[b] ? 1 : 0);
     double tq = tan(0.5 * phi), sq = sin(phi);
     if (neg) { tq = -tq; sq = -sq; }
     row[pos] = make_float2((float)tq, (float)sq);
@@ -297,8 +318,8 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
 // (1, 0) on the other. ab[rho][slot] = (alpha, beta): the dphi weights, w = alpha z_t + beta z_b
 // = cos(th_r) z_i + sigma_i sigma_j sin(th_r) z_j, th_r the pi-reduced angle.
 __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ theta, const float *__restrict__ phi,
-                         const uint8_t *__restrict__ mask, const uint8_t *__restrict__ sig, float4 *__restrict__ ph,
-                         float2 *__restrict__ ab) {
+                         const uint8_t *__restrict__ mask, const uint8_t *__restrict__ sig,
+                         const int32_t *__restrict__ lay, float4 *__restrict__ ph, float2 *__restrict__ ab) {
     int S = ne / 2, R = ne - 1;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)(R + 2) * S) return;
@@ -315,13 +336,13 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
     }
     int r = rho - 1;
     int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);
-    int64_t f = flat_of(r, k, n, ne);
+    int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
     bool active = f >= 0 && (!mask || mask[f]);
     double th = active ? (double)theta[f] : 0.0, pv = active ? (double)phi[f] : 0.0;
     double thr = th;
     if (fabs(th) > 1.5707963267948966) thr = th - copysign(3.141592653589793, th);
     float pc = (float)cos(pv), ps = (float)sin(pv);
-    bool top_is_i = a < b;
+    bool top_is_i = lay[a] < lay[b];
     phr[pos_ph] = top_is_i ? make_float4(pc, ps, 1.f, 0.f) : make_float4(1.f, 0.f, pc, ps);
     double cr = cos(thr), sr = sin(thr);
     if (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) sr = -sr;
@@ -389,6 +410,7 @@ struct GenArgs {
     const float4 *coef_ph;  // unitary: phases per slot, natural order
     const float2 *coef_ab;  // unitary backward: dphi weights per slot, natural order
     const uint8_t *sfin;
+    const int32_t *lrow;  // row of each label (start permutation)
     float *partial;
     float *scratch;  // [ne][G*32] (Z) and, for BWD, another [ne][G*32] (D); float2 entries when unitary
     int64_t nslabs;
@@ -408,12 +430,13 @@ __global__ void __launch_bounds__(32) k_generic(const GenArgs a) {
     for (int64_t slab = blockIdx.x; slab < a.nslabs; slab += gridDim.x, slab_i++) {
         const int64_t col = slab * 32 + lane;
         const bool live = col < a.m;
-        for (int i = 0; i < ne; i++) {
+        for (int i = 0; i < ne; i++) {  // i: label, row = lrow[i]
             float v = 0.f, d = 0.f;
-            if (i < n && live) {
-                if (MODE == M_BUILDU) v = (col == i) ? 1.f : 0.f;
-                else v = a.X[(int64_t)i * a.ldx + col];
-                if (GRAD) d = a.dY[(int64_t)i * a.lddy + col];
+            const int row = a.lrow[i];
+            if (row < n && live) {
+                if (MODE == M_BUILDU) v = (col == row) ? 1.f : 0.f;
+                else v = a.X[(int64_t)row * a.ldx + col];
+                if (GRAD) d = a.dY[(int64_t)row * a.lddy + col];
                 if (UP && a.sfin[i]) { v = -v; d = -d; }
             }
             Z[(int64_t)i * stride] = v;
@@ -448,10 +471,12 @@ __global__ void __launch_bounds__(32) k_generic(const GenArgs a) {
             }
         }
         if (live && !(GRAD && a.Y == nullptr)) {
-            for (int i = 0; i < n; i++) {
+            for (int i = 0; i < ne; i++) {
+                const int row = a.lrow[i];
+                if (row >= n) continue;
                 float v = GRAD ? D[(int64_t)i * stride] : Z[(int64_t)i * stride];
                 if (!UP && a.sfin[i]) v = -v;
-                a.Y[(int64_t)i * a.ldy + col] = v;
+                a.Y[(int64_t)row * a.ldy + col] = v;
             }
         }
     }
@@ -479,12 +504,14 @@ __global__ void __launch_bounds__(32) k_generic_u(const GenArgs a) {
     for (int64_t slab = blockIdx.x; slab < a.nslabs; slab += gridDim.x, slab_i++) {
         const int64_t col = slab * 32 + lane;
         const bool live = col < mc;
-        for (int i = 0; i < ne; i++) {
+        for (int i = 0; i < ne; i++) {  // i: label, row = lrow[i]
             float2 v = make_float2(0.f, 0.f), d = make_float2(0.f, 0.f);
-            if (i < n && live) {
-                if (BM == M_BUILDU) v.x = (col == i) ? 1.f : 0.f;
-                else v = make_float2(a.X[(int64_t)i * a.ldx + 2 * col], a.X[(int64_t)i * a.ldx + 2 * col + 1]);
-                if (GRAD) d = make_float2(a.dY[(int64_t)i * a.lddy + 2 * col], a.dY[(int64_t)i * a.lddy + 2 * col + 1]);
+            const int row = a.lrow[i];
+            if (row < n && live) {
+                if (BM == M_BUILDU) v.x = (col == row) ? 1.f : 0.f;
+                else v = make_float2(a.X[(int64_t)row * a.ldx + 2 * col], a.X[(int64_t)row * a.ldx + 2 * col + 1]);
+                if (GRAD)
+                    d = make_float2(a.dY[(int64_t)row * a.lddy + 2 * col], a.dY[(int64_t)row * a.lddy + 2 * col + 1]);
                 if (UP && a.sfin[i]) { v = neg_v(v); d = neg_v(d); }
             }
             Z[(int64_t)i * stride] = v;
@@ -543,11 +570,13 @@ __global__ void __launch_bounds__(32) k_generic_u(const GenArgs a) {
             }
         }
         if (live && !(GRAD && a.Y == nullptr)) {
-            for (int i = 0; i < n; i++) {
+            for (int i = 0; i < ne; i++) {
+                const int row = a.lrow[i];
+                if (row >= n) continue;
                 float2 v = GRAD ? D[(int64_t)i * stride] : Z[(int64_t)i * stride];
                 if (!UP && a.sfin[i]) v = neg_v(v);
-                a.Y[(int64_t)i * a.ldy + 2 * col] = v.x;
-                a.Y[(int64_t)i * a.ldy + 2 * col + 1] = v.y;
+                a.Y[(int64_t)row * a.ldy + 2 * col] = v.x;
+                a.Y[(int64_t)row * a.ldy + 2 * col + 1] = v.y;
             }
         }
     }
@@ -675,21 +704,31 @@ int launch_ring(int mode, const Cfg &c, RingArgs &ra, int64_t grid, cudaStream_t
     return 0;
 }
 
+// Layout options (start permutation, reflection); perm is a device int32[n_eff] or NULL.
+struct Lay {
+    const int32_t *perm;
+    int refl;
+};
+constexpr Lay kNoLay{nullptr, -1};
+
 int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask, uint8_t *ws, const WsLayout &L,
-                   cudaStream_t st, const float *phi = nullptr) {
+                   cudaStream_t st, const float *phi = nullptr, Lay lo = kNoLay) {
     int64_t RS = (int64_t)c.R * c.S;
-    k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, ws + L.flip);
+    int32_t *lay = reinterpret_cast<int32_t *>(ws + L.lay);
+    k_layout<<<1, 1024, 0, st>>>(n, c.ne, lo.perm, lo.refl, lay);
     CUDA_TRY(cudaGetLastError());
-    k_sigma<<<(unsigned)((c.ne + 7) / 8), 256, 0, st>>>(c.ne, ws + L.flip, ws + L.sig, ws + L.sfin);
+    k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, lay, ws + L.flip);
+    CUDA_TRY(cudaGetLastError());
+    k_sigma<<<(unsigned)((c.ne + 7) / 8), 256, 0, st>>>(c.ne, ws + L.flip, lay, ws + L.sig, ws + L.sfin);
     CUDA_TRY(cudaGetLastError());
     int64_t tot = (int64_t)(c.R + 2) * c.S;
     int W = c.fast ? c.W : c.S, Lq = c.fast ? c.La : 1;
     k_coef<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, c.rowbytes, theta, mask, ws + L.flip,
-                                                          ws + L.sig, ws + L.coef,
+                                                          ws + L.sig, lay, ws + L.coef,
                                                           reinterpret_cast<int32_t *>(ws + L.amap));
     CUDA_TRY(cudaGetLastError());
     if (phi) {
-        k_coef_u<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, theta, phi, mask, ws + L.sig,
+        k_coef_u<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, theta, phi, mask, ws + L.sig, lay,
                                                                 reinterpret_cast<float4 *>(ws + L.coef_ph),
                                                                 reinterpret_cast<float2 *>(ws + L.coef_ab));
         CUDA_TRY(cudaGetLastError());
@@ -726,6 +765,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
         ra.n = n; ra.ne = c.ne; ra.La = c.La;
         ra.m = m; ra.X = X; ra.ldx = ldx; ra.dY = dY; ra.lddy = lddy; ra.Y = Y; ra.ldy = ldy;
         ra.coef = ws + L.coef; ra.sfin = ws + L.sfin;
+        ra.lrow = reinterpret_cast<const int32_t *>(ws + L.lay);
         ra.coef_ph = ws + L.coef_ph; ra.coef_ab = ws + L.coef_ab;
         ra.partial = reinterpret_cast<float *>(ws + L.partial);
         ra.nslabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
@@ -737,6 +777,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
     ga.n = n; ga.ne = c.ne; ga.S = c.S; ga.rowbytes = c.rowbytes; ga.m = m;
     ga.X = X; ga.ldx = ldx; ga.dY = dY; ga.lddy = lddy; ga.Y = Y; ga.ldy = ldy;
     ga.coef = ws + L.coef; ga.sfin = ws + L.sfin;
+    ga.lrow = reinterpret_cast<const int32_t *>(ws + L.lay);
     ga.coef_ph = reinterpret_cast<const float4 *>(ws + L.coef_ph);
     ga.coef_ab = reinterpret_cast<const float2 *>(ws + L.coef_ab);
     ga.partial = reinterpret_cast<float *>(ws + L.partial);
@@ -769,33 +810,62 @@ int64_t givens_num_angles(int32_t n) { return n < 2 ? -1 : (int64_t)n * (n - 1) 
 
 int givens_supported(int32_t n) { return (n >= 2 && n <= 32768) ? 1 : 0; }
 
-int givens_schedule(int32_t n, int32_t *pairs_host, int64_t *flat_host) {
-    if (n < 2) return fail(GIVENS_EINVAL, "n must be >= 2 (got %d)", n);
+int givens_check_perm(int32_t n, const int32_t *perm_host) {
+    if (n < 2 || n > 32768) return fail(GIVENS_EINVAL, "n must be in [2, 32768] (got %d)", n);
+    if (!perm_host) return 0;
+    const int ne = n + (n & 1);
+    std::string seen((size_t)ne, '\0');
+    for (int l = 0; l < ne; l++) {
+        int v = perm_host[l];
+        if (v < 0 || v >= ne) return fail(GIVENS_EINVAL, "perm[%d] = %d out of range [0, %d)", l, v, ne);
+        if (seen[(size_t)v]) return fail(GIVENS_EINVAL, "perm has a duplicate entry %d", v);
+        seen[(size_t)v] = 1;
+    }
+    return 0;
+}
+
+int givens_schedule_ex(int32_t n, const int32_t *perm_host, int32_t *pairs_host, int64_t *flat_host) {
+    int rc = givens_check_perm(n, perm_host);
+    if (rc) return rc;
     int ne = n + (n & 1), S = ne / 2, R = ne - 1;
+    int64_t f = 0;
     for (int r = 0; r < R; r++)
         for (int k = 0; k < S; k++) {
-            int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);
+            int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);  // labels
+            if (perm_host) { a = perm_host[a]; b = perm_host[b]; }
             int64_t q = (int64_t)r * S + k;
             if (pairs_host) {
                 pairs_host[2 * q] = a < b ? a : b;
                 pairs_host[2 * q + 1] = a < b ? b : a;
             }
-            if (flat_host) flat_host[q] = flat_of(r, k, n, ne);
+            int64_t idx = (a == n || b == n) ? -1 : f++;  // block-major, byes skipped
+            if (flat_host) flat_host[q] = idx;
+        }
+    return 0;
+}
+
+int givens_schedule(int32_t n, int32_t *pairs_host, int64_t *flat_host) {
+    return givens_schedule_ex(n, nullptr, pairs_host, flat_host);
+}
+
+int givens_mask_from_dims_ex(int32_t n, const int32_t *perm_host, const uint8_t *excl, uint8_t *mask) {
+    if (n < 2 || !excl || !mask) return fail(GIVENS_EINVAL, "bad arguments");
+    int rc = givens_check_perm(n, perm_host);
+    if (rc) return rc;
+    int ne = n + (n & 1), S = ne / 2, R = ne - 1;
+    int64_t f = 0;
+    for (int r = 0; r < R; r++)
+        for (int k = 0; k < S; k++) {
+            int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);
+            if (perm_host) { a = perm_host[a]; b = perm_host[b]; }
+            if (a == n || b == n) continue;
+            mask[f++] = (excl[a] && excl[b]) ? 0 : 1;
         }
     return 0;
 }
 
 int givens_mask_from_dims(int32_t n, const uint8_t *excl, uint8_t *mask) {
-    if (n < 2 || !excl || !mask) return fail(GIVENS_EINVAL, "bad arguments");
-    int ne = n + (n & 1), S = ne / 2, R = ne - 1;
-    for (int r = 0; r < R; r++)
-        for (int k = 0; k < S; k++) {
-            int64_t f = flat_of(r, k, n, ne);
-            if (f < 0) continue;
-            int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);
-            mask[f] = (excl[a] && excl[b]) ? 0 : 1;
-        }
-    return 0;
+    return givens_mask_from_dims_ex(n, nullptr, excl, mask);
 }
 
 size_t givens_workspace_bytes(int op, int32_t n, int64_t m) {
@@ -806,10 +876,11 @@ size_t givens_workspace_bytes(int op, int32_t n, int64_t m) {
 
 int givens_u_supported(int32_t n) { return (n >= 2 && n <= 32768) ? 1 : 0; }
 
-int givens_u_apply(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const float *X,
-                   int64_t ldx, float *Y, int64_t ldy, int adjoint, void *ws, size_t ws_bytes, void *stream) {
+int givens_u_apply_ex(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const float *X,
+                   int64_t ldx, float *Y, int64_t ldy, int adjoint, const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes, void *stream) {
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_U_APPLY);
     if (rc) return rc;
+    if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
     if (!theta || !phi || !X || !Y) return fail(GIVENS_EINVAL, "theta, phi, X and Y must be non-NULL");
     if (ldx < m || ldy < m) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (X == Y && ldx != ldy) return fail(GIVENS_EINVAL, "in-place apply needs ldx == ldy");
@@ -817,31 +888,33 @@ int givens_u_apply(int32_t n, int64_t m, const float *theta, const float *phi, c
     WsLayout L = ws_layout(c, GIVENS_OP_U_APPLY, m);
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
-    if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi))) return rc;
+    if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
     // a complex column is two interleaved real columns
     return run_apply_mode((adjoint ? M_TRANS : M_FWD) | M_UNI, n, 2 * m, X, 2 * ldx, nullptr, 0, Y, 2 * ldy, w, L,
                           c, st);
 }
 
-int givens_u_build_U(int32_t n, const float *theta, const float *phi, const uint8_t *mask, float *U, int64_t ldu,
-                     void *ws, size_t ws_bytes, void *stream) {
+int givens_u_build_U_ex(int32_t n, const float *theta, const float *phi, const uint8_t *mask, float *U, int64_t ldu,
+                     const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes, void *stream) {
     int rc = check_common(n, n, ws, ws_bytes, GIVENS_OP_U_BUILD_U);
     if (rc) return rc;
+    if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
     if (!theta || !phi || !U) return fail(GIVENS_EINVAL, "theta, phi and U must be non-NULL");
     if (ldu < n) return fail(GIVENS_EINVAL, "ldu < n");
     Cfg c = make_cfg_u(n);
     WsLayout L = ws_layout(c, GIVENS_OP_U_BUILD_U, n);
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
-    if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi))) return rc;
+    if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
     return run_apply_mode(M_BUILDU | M_UNI, n, 2 * (int64_t)n, nullptr, 0, nullptr, 0, U, 2 * ldu, w, L, c, st);
 }
 
-int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
+int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
                       const float *Y, int64_t ldy, const float *dY, int64_t lddy, float *dX, int64_t lddx,
-                      float *dtheta, float *dphi, int flags, void *ws, size_t ws_bytes, void *stream) {
+                      float *dtheta, float *dphi, int flags, const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes, void *stream) {
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_U_BACKWARD);
     if (rc) return rc;
+    if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
     if (!theta || !phi || !Y || !dY || !dtheta || !dphi)
         return fail(GIVENS_EINVAL, "theta, phi, Y, dY, dtheta and dphi must be non-NULL");
     if (ldy < m || lddy < m || (dX && lddx < m)) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
@@ -851,7 +924,7 @@ int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
     if (flags & GIVENS_FLAG_RECOMPUTE) {
-        if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi))) return rc;
+        if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
     }
     int64_t N = givens_num_angles(n);
     if (m == 0) {
@@ -869,10 +942,11 @@ int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi
     return 0;
 }
 
-int givens_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
-                 float *Y, int64_t ldy, int transpose, void *ws, size_t ws_bytes, void *stream) {
+int givens_apply_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
+                 float *Y, int64_t ldy, int transpose, const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes, void *stream) {
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_APPLY);
     if (rc) return rc;
+    if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
     if (!theta || !X || !Y) return fail(GIVENS_EINVAL, "theta, X and Y must be non-NULL");
     if (ldx < m || ldy < m) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (X == Y && ldx != ldy) return fail(GIVENS_EINVAL, "in-place apply needs ldx == ldy");
@@ -880,29 +954,32 @@ int givens_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, 
     WsLayout L = ws_layout(c, GIVENS_OP_APPLY, m);
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
-    if ((rc = run_precompute(c, n, theta, mask, w, L, st))) return rc;
+    if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
     return run_apply_mode(transpose ? M_TRANS : M_FWD, n, m, X, ldx, nullptr, 0, Y, ldy, w, L, c, st);
 }
 
-int givens_build_U(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu, void *ws,
+int givens_build_U_ex(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu,
+                      const int32_t *perm, int32_t reflect_col, void *ws,
                    size_t ws_bytes, void *stream) {
     int rc = check_common(n, n, ws, ws_bytes, GIVENS_OP_BUILD_U);
     if (rc) return rc;
+    if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
     if (!theta || !U) return fail(GIVENS_EINVAL, "theta and U must be non-NULL");
     if (ldu < n) return fail(GIVENS_EINVAL, "ldu < n");
     Cfg c = make_cfg(n);
     WsLayout L = ws_layout(c, GIVENS_OP_BUILD_U, n);
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
-    if ((rc = run_precompute(c, n, theta, mask, w, L, st))) return rc;
+    if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
     return run_apply_mode(M_BUILDU, n, n, nullptr, 0, nullptr, 0, U, ldu, w, L, c, st);
 }
 
-int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *Y, int64_t ldy,
-                    const float *dY, int64_t lddy, float *dX, int64_t lddx, float *dtheta, int flags, void *ws,
+int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *Y, int64_t ldy,
+                    const float *dY, int64_t lddy, float *dX, int64_t lddx, float *dtheta, int flags, const int32_t *perm, int32_t reflect_col, void *ws,
                     size_t ws_bytes, void *stream) {
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_BACKWARD);
     if (rc) return rc;
+    if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
     if (!theta || !Y || !dY || !dtheta) return fail(GIVENS_EINVAL, "theta, Y, dY and dtheta must be non-NULL");
     if (ldy < m || lddy < m || (dX && lddx < m)) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (dX && dX == dY && lddx != lddy) return fail(GIVENS_EINVAL, "in-place dX needs lddx == lddy");
@@ -911,7 +988,7 @@ int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
     if (flags & GIVENS_FLAG_RECOMPUTE) {
-        if ((rc = run_precompute(c, n, theta, mask, w, L, st))) return rc;
+        if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
     }
     int64_t N = givens_num_angles(n);
     if (m == 0) {
@@ -926,6 +1003,36 @@ int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mas
         dtheta, nullptr);
     CUDA_TRY(cudaGetLastError());
     return 0;
+}
+
+// ------------------------------------------------------------------ identity-layout entry points
+int givens_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
+                 float *Y, int64_t ldy, int transpose, void *ws, size_t ws_bytes, void *stream) {
+    return givens_apply_ex(n, m, theta, mask, X, ldx, Y, ldy, transpose, nullptr, -1, ws, ws_bytes, stream);
+}
+int givens_build_U(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu, void *ws,
+                   size_t ws_bytes, void *stream) {
+    return givens_build_U_ex(n, theta, mask, U, ldu, nullptr, -1, ws, ws_bytes, stream);
+}
+int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *Y, int64_t ldy,
+                    const float *dY, int64_t lddy, float *dX, int64_t lddx, float *dtheta, int flags, void *ws,
+                    size_t ws_bytes, void *stream) {
+    return givens_backward_ex(n, m, theta, mask, Y, ldy, dY, lddy, dX, lddx, dtheta, flags, nullptr, -1, ws,
+                              ws_bytes, stream);
+}
+int givens_u_apply(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask, const float *X,
+                   int64_t ldx, float *Y, int64_t ldy, int adjoint, void *ws, size_t ws_bytes, void *stream) {
+    return givens_u_apply_ex(n, m, theta, phi, mask, X, ldx, Y, ldy, adjoint, nullptr, -1, ws, ws_bytes, stream);
+}
+int givens_u_build_U(int32_t n, const float *theta, const float *phi, const uint8_t *mask, float *U, int64_t ldu,
+                     void *ws, size_t ws_bytes, void *stream) {
+    return givens_u_build_U_ex(n, theta, phi, mask, U, ldu, nullptr, -1, ws, ws_bytes, stream);
+}
+int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
+                      const float *Y, int64_t ldy, const float *dY, int64_t lddy, float *dX, int64_t lddx,
+                      float *dtheta, float *dphi, int flags, void *ws, size_t ws_bytes, void *stream) {
+    return givens_u_backward_ex(n, m, theta, phi, mask, Y, ldy, dY, lddy, dX, lddx, dtheta, dphi, flags, nullptr, -1,
+                                ws, ws_bytes, stream);
 }
 
 int givens_index_trace(int32_t n, int direction, int32_t *out_dev, void *stream) {

@@ -40,6 +40,14 @@ __device__ __forceinline__ float cross_acc(float acc, float2 db, float2 zt, floa
     float2 s2 = __ffma2_rn(neg_v(dt), zb, __fmul2_rn(db, zt));
     return acc + (s2.x + s2.y);
 }
+// the first term of a sum: no "0 + x" (an FADD the compiler must keep, 0 + -0 = +0)
+__device__ __forceinline__ float cross_first(float db, float zt, float dt, float zb) {
+    return fmaf(-dt, zb, db * zt);
+}
+__device__ __forceinline__ float cross_first(float2 db, float2 zt, float2 dt, float2 zb) {
+    float2 s2 = __ffma2_rn(neg_v(dt), zb, __fmul2_rn(db, zt));
+    return s2.x + s2.y;
+}
 
 // dphi accumulation of the unitary backward: acc + Re(i conj(v) w) = acc + v.im w.re - v.re w.im
 __device__ __forceinline__ float phi_acc(float acc, float2 v, float2 w) {

@@ -27,28 +27,72 @@ def n_eff(n: int) -> int:
     return n + (n % 2)
 
 
-def schedule(n: int):
-    """Circle-method schedule (closed form, host side): pairs int32[R][S][2], flat int64[R][S]."""
+def _np_ptr(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+class Layout:
+    """Layout options of one n: the circle method's start permutation
+    (a permutation of 0..n_eff-1, None = identity) and the reflection
+    class (column `reflect_col` of U negated, det -1). The permutation is
+    checked once on the host here (givens_check_perm) and kept on the device for the kernels."""
+
+    def __init__(self, n: int, perm=None, reflect_col: int | None = None, device=None):
+        self.n = int(n)
+        self.reflect_col = -1 if reflect_col is None else int(reflect_col)
+        if not -1 <= self.reflect_col < self.n:
+            raise ValueError(f"reflect_col must be None or in [0, {n}) (got {reflect_col})")
+        self.perm_host = None
+        self.perm = None
+        if perm is not None:
+            p = np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+            if p.shape != (n_eff(n),):
+                raise ValueError(f"perm must have n_eff = {n_eff(n)} entries (got {p.shape})")
+            check(lib().givens_check_perm(n, _np_ptr(p)))
+            self.perm_host = p
+            self.perm = torch.from_numpy(p).to(device or "cuda")
+
+    def args(self, n: int, device):
+        if n != self.n:
+            raise ValueError(f"layout is for n={self.n}, not n={n}")
+        if self.perm is not None and self.perm.device != torch.device(device):
+            self.perm = self.perm.to(device)
+        return (None if self.perm is None else ctypes.c_void_p(self.perm.data_ptr())), self.reflect_col
+
+
+def _lay(layout, n, device):
+    return (None, -1) if layout is None else layout.args(n, device)
+
+
+def schedule(n: int, perm=None):
+    """Circle-method schedule (closed form, host side): pairs int32[R][S][2], flat int64[R][S];
+    perm = start permutation of 0..n_eff-1 (None = identity)."""
     ne = n_eff(n)
     R, S = ne - 1, ne // 2
     pairs = np.zeros((R, S, 2), dtype=np.int32)
     flat = np.zeros((R, S), dtype=np.int64)
-    check(lib().givens_schedule(n, pairs.ctypes.data_as(ctypes.c_void_p), flat.ctypes.data_as(ctypes.c_void_p)))
+    p = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    if p is not None and p.shape != (ne,):
+        raise ValueError(f"perm must have n_eff = {ne} entries")
+    check(lib().givens_schedule_ex(n, _np_ptr(p), _np_ptr(pairs), _np_ptr(flat)))
     return pairs, flat
 
 
-def mask_from_dims(n: int, excluded) -> np.ndarray:
+def mask_from_dims(n: int, excluded, perm=None) -> np.ndarray:
     """uint8 mask[N]: pair (i,j) pinned iff both i and j are in the excluded dimension set."""
     ex = np.zeros(n, dtype=np.uint8)
     ex[np.asarray(list(excluded), dtype=np.int64)] = 1
     mask = np.zeros(num_angles(n), dtype=np.uint8)
-    check(lib().givens_mask_from_dims(n, ex.ctypes.data_as(ctypes.c_void_p), mask.ctypes.data_as(ctypes.c_void_p)))
+    p = None if perm is None else np.ascontiguousarray(np.asarray(perm, dtype=np.int32))
+    if p is not None and p.shape != (n_eff(n),):
+        raise ValueError(f"perm must have n_eff = {n_eff(n)} entries")
+    check(lib().givens_mask_from_dims_ex(n, _np_ptr(p), _np_ptr(ex), _np_ptr(mask)))
     return mask
 
 
-def mask_from_keep(n: int, m_keep: int) -> np.ndarray:
+def mask_from_keep(n: int, m_keep: int, perm=None) -> np.ndarray:
     """Paper §5: exclude every pair inside {m_keep, ..., n-1}."""
-    return mask_from_dims(n, range(m_keep, n))
+    return mask_from_dims(n, range(m_keep, n), perm=perm)
 
 
 def workspace_bytes(op: int, n: int, m: int) -> int:
@@ -86,7 +130,7 @@ def _check_theta(theta, mask, n):
 
 
 def apply(theta: torch.Tensor, X: torch.Tensor, mask: torch.Tensor | None = None, transpose: bool = False,
-          out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+          out: torch.Tensor | None = None, ws: torch.Tensor | None = None, layout: Layout | None = None) -> torch.Tensor:
     """Y = U(theta) X (or U^T X): Algorithm 2 on the columns of X."""
     n, m = X.shape
     _check_matrix("X", X, n)
@@ -95,27 +139,28 @@ def apply(theta: torch.Tensor, X: torch.Tensor, mask: torch.Tensor | None = None
     _check_matrix("out", Y, n)
     if ws is None:
         ws = workspace(OP_APPLY, n, m, X.device)
-    check(lib().givens_apply(n, m, _ptr(theta), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y), Y.stride(0),
-                             int(bool(transpose)), _ptr(ws), ws.numel(), _stream(X.device)))
+    check(lib().givens_apply_ex(n, m, _ptr(theta), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y), Y.stride(0),
+                                int(bool(transpose)), *_lay(layout, n, X.device), _ptr(ws), ws.numel(),
+                                _stream(X.device)))
     return Y
 
 
 def build_U(theta: torch.Tensor, n: int, mask: torch.Tensor | None = None, out: torch.Tensor | None = None,
-            ws: torch.Tensor | None = None) -> torch.Tensor:
+            ws: torch.Tensor | None = None, layout: Layout | None = None) -> torch.Tensor:
     """U = U(theta) (Algorithm 2 from U <- I_n)."""
     _check_theta(theta, mask, n)
     U = torch.empty((n, n), dtype=torch.float32, device=theta.device) if out is None else out
     _check_matrix("U", U, n)
     if ws is None:
         ws = workspace(OP_BUILD_U, n, n, theta.device)
-    check(lib().givens_build_U(n, _ptr(theta), _ptr(mask), _ptr(U), U.stride(0), _ptr(ws), ws.numel(),
-                               _stream(theta.device)))
+    check(lib().givens_build_U_ex(n, _ptr(theta), _ptr(mask), _ptr(U), U.stride(0), *_lay(layout, n, theta.device),
+                                  _ptr(ws), ws.numel(), _stream(theta.device)))
     return U
 
 
 def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch.Tensor | None = None,
              want_dX: bool = True, ws: torch.Tensor | None = None, recompute: bool = True,
-             dtheta: torch.Tensor | None = None, dX: torch.Tensor | None = None):
+             dtheta: torch.Tensor | None = None, dX: torch.Tensor | None = None, layout: Layout | None = None):
     """(dtheta, dX) for Y = U(theta) X given Y and dY (replay backward, §4).
 
     recompute=False reuses the coefficient tables a preceding apply/build_U left in `ws`
@@ -133,9 +178,10 @@ def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch
         dX = torch.empty_like(dY)
     if dX is not None:
         _check_matrix("dX", dX, n)
-    check(lib().givens_backward(n, m, _ptr(theta), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY), dY.stride(0),
-                                _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
-                                FLAG_RECOMPUTE if recompute else 0, _ptr(ws), ws.numel(), _stream(Y.device)))
+    check(lib().givens_backward_ex(n, m, _ptr(theta), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY), dY.stride(0),
+                                   _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
+                                   FLAG_RECOMPUTE if recompute else 0, *_lay(layout, n, Y.device), _ptr(ws),
+                                   ws.numel(), _stream(Y.device)))
     return dtheta, dX
 
 
@@ -152,10 +198,11 @@ class GivensApply(torch.autograd.Function):
     backward-sized workspace and reused by the backward (no recompute)."""
 
     @staticmethod
-    def forward(ctx, theta, X, mask=None):
+    def forward(ctx, theta, X, mask=None, layout=None):
         n, m = X.shape
         ws = workspace(OP_BACKWARD, n, m, X.device)
-        Y = apply(theta, X, mask=mask, ws=ws)
+        Y = apply(theta, X, mask=mask, ws=ws, layout=layout)
+        ctx.layout = layout
         ctx.save_for_backward(theta, Y, mask if mask is not None else torch.empty(0, device=X.device))
         ctx.ws = ws
         ctx.has_mask = mask is not None
@@ -166,13 +213,14 @@ class GivensApply(torch.autograd.Function):
         theta, Y, mask = ctx.saved_tensors
         mask = mask if ctx.has_mask else None
         dY = dY.contiguous()
-        dtheta, dX = backward(theta, Y, dY, mask=mask, want_dX=ctx.needs_input_grad[1], ws=ctx.ws, recompute=False)
-        return dtheta, dX, None
+        dtheta, dX = backward(theta, Y, dY, mask=mask, want_dX=ctx.needs_input_grad[1], ws=ctx.ws, recompute=False,
+                              layout=ctx.layout)
+        return dtheta, dX, None, None
 
 
-def givens_apply(theta, X, mask=None):
+def givens_apply(theta, X, mask=None, layout=None):
     """Differentiable Y = U(theta) X."""
-    return GivensApply.apply(theta, X, mask)
+    return GivensApply.apply(theta, X, mask, layout)
 
 
 def version() -> str:
@@ -250,7 +298,7 @@ def _check_phi(phi, n):
         raise ValueError(f"phi must be a contiguous CUDA float32 tensor of {N} phase angles")
 
 
-def u_apply(theta, phi, X, mask=None, adjoint: bool = False, out=None, ws=None):
+def u_apply(theta, phi, X, mask=None, adjoint: bool = False, out=None, ws=None, layout: Layout | None = None):
     """Y = U(theta, phi) X or U^dagger X (Algorithm 4), X complex64 [n, m]."""
     n, m = X.shape
     _check_cmatrix("X", X, n)
@@ -260,12 +308,13 @@ def u_apply(theta, phi, X, mask=None, adjoint: bool = False, out=None, ws=None):
     _check_cmatrix("out", Y, n)
     if ws is None:
         ws = workspace(OP_U_APPLY, n, m, X.device)
-    check(lib().givens_u_apply(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y),
-                               Y.stride(0), int(bool(adjoint)), _ptr(ws), ws.numel(), _stream(X.device)))
+    check(lib().givens_u_apply_ex(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y),
+                                  Y.stride(0), int(bool(adjoint)), *_lay(layout, n, X.device), _ptr(ws), ws.numel(),
+                                  _stream(X.device)))
     return Y
 
 
-def u_build_U(theta, phi, n: int, mask=None, out=None, ws=None):
+def u_build_U(theta, phi, n: int, mask=None, out=None, ws=None, layout: Layout | None = None):
     """U = U(theta, phi) in U(n), complex64 [n, n]."""
     _check_theta(theta, mask, n)
     _check_phi(phi, n)
@@ -273,12 +322,13 @@ def u_build_U(theta, phi, n: int, mask=None, out=None, ws=None):
     _check_cmatrix("U", U, n)
     if ws is None:
         ws = workspace(OP_U_BUILD_U, n, n, theta.device)
-    check(lib().givens_u_build_U(n, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(U), U.stride(0), _ptr(ws), ws.numel(),
-                                 _stream(theta.device)))
+    check(lib().givens_u_build_U_ex(n, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(U), U.stride(0),
+                                    *_lay(layout, n, theta.device), _ptr(ws), ws.numel(), _stream(theta.device)))
     return U
 
 
-def u_backward(theta, phi, Y, dY, mask=None, want_dX: bool = True, ws=None, recompute: bool = True):
+def u_backward(theta, phi, Y, dY, mask=None, want_dX: bool = True, ws=None, recompute: bool = True,
+               layout: Layout | None = None):
     """(dtheta, dphi, dX) for a real loss of Y = U X, dY = dL/dRe(Y) + i dL/dIm(Y)."""
     n, m = Y.shape
     _check_cmatrix("Y", Y, n)
@@ -292,8 +342,8 @@ def u_backward(theta, phi, Y, dY, mask=None, want_dX: bool = True, ws=None, reco
     dtheta = torch.empty(N, dtype=torch.float32, device=Y.device)
     dphi = torch.empty(N, dtype=torch.float32, device=Y.device)
     dX = torch.empty_like(dY) if want_dX else None
-    check(lib().givens_u_backward(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY),
-                                  dY.stride(0), _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
-                                  _ptr(dphi), FLAG_RECOMPUTE if recompute else 0, _ptr(ws), ws.numel(),
-                                  _stream(Y.device)))
+    check(lib().givens_u_backward_ex(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY),
+                                     dY.stride(0), _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
+                                     _ptr(dphi), FLAG_RECOMPUTE if recompute else 0, *_lay(layout, n, Y.device),
+                                     _ptr(ws), ws.numel(), _stream(Y.device)))
     return dtheta, dphi, dX

@@ -100,3 +100,45 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", src).replace("oracle/", ""), f
+
+
+# ---------------------------------------------------------------- layout options (§8(f3))
+
+def _rperm(n, seed):
+    return np.random.default_rng(seed).permutation(n + n % 2).astype(np.int32)
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 6, 7, 16, 33, 64, 129, 1024, 2047])
+@pytest.mark.parametrize("seed", [0, 1])
+def test_permuted_schedule_equals_literal(g, n, seed):
+    """Host closed form + relabeling == the oracle's literal circle method from the permuted
+    start sequence (bit-exact), including where the odd-n bye lands."""
+    p = _rperm(n, seed)
+    p1, f1 = g.schedule(n, perm=p)
+    p2, f2 = oracle.schedule(n, perm=p)
+    assert (p1 == p2).all() and (f1 == f2).all()
+
+
+@pytest.mark.parametrize("n,mk", [(8, 4), (9, 3), (64, 17), (2047, 1024)])
+def test_permuted_mask_matches_oracle(g, n, mk):
+    p = _rperm(n, n)
+    assert (g.mask_from_keep(n, mk, perm=p) == oracle.mask_from_keep(n, mk, perm=p)).all()
+
+
+def test_layout_validation(g):
+    with pytest.raises(g.GivensError):
+        g.Layout(6, perm=[0, 1, 2, 3, 4, 4], device="cpu")
+    with pytest.raises(g.GivensError):
+        g.Layout(5, perm=[0, 1, 2, 3, 6, 5], device="cpu")
+    with pytest.raises(ValueError):
+        g.Layout(5, perm=[0, 1, 2, 3, 4], device="cpu")  # n_eff = 6 entries needed
+    with pytest.raises(ValueError):
+        g.Layout(5, reflect_col=5, device="cpu")
+    lay = g.Layout(5, perm=[5, 0, 1, 2, 3, 4], reflect_col=4, device="cpu")
+    assert lay.reflect_col == 4 and lay.perm_host.tolist() == [5, 0, 1, 2, 3, 4]
+    from paper_2106_00003_b200 import _lib
+    L = _lib.lib()
+    # reflect_col out of range is a parameter error, detected before anything is enqueued
+    rc = L.givens_apply_ex(8, 4, None, None, None, 4, None, 4, 0, None, 8, ctypes.c_void_p(256), 10 ** 9, None)
+    assert rc == _lib.EINVAL
+    assert b"reflect_col" in L.givens_last_error()
