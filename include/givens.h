@@ -204,6 +204,27 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
                          float *dtheta, float *dphi, int flags, const int32_t *perm, int32_t reflect_col,
                          void *ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------------------------------
+ * GEMM path: the paper's own framing of the workload --
+ * build U(theta) once (Alg. 2 from I on the register ring), then Y = U X (or U^T X) as a dense
+ * GEMM on the tensor cores in 3xTF32 (hi/lo split of both operands, three TF32 products,
+ * relative error ~2^-21), and for the backward dX = U^T dY, Gamma = dL/dU =
+ * dY X^T = (dY Y^T) U and dtheta = Algorithm 3 on Gamma (computed by the
+ * replay backward with X = I). Same argument meanings, layout options and results as
+ * givens_apply_ex / givens_backward_ex (within the fp32 tolerances), but: the workspace is
+ * givens_gemm_workspace_bytes(n, m) (it holds U and the hi/lo splits: ~4 n m floats), the GEMMs
+ * run in cuBLAS (libcublas.so.12, loaded at first use; GIVENS_EUNSUPPORTED if absent; cuBLAS
+ * allocates its own handle/workspace once per thread and device), and nothing may alias.
+ * givens_gemm_backward without GIVENS_FLAG_RECOMPUTE reuses the U a givens_gemm_apply left in ws.
+ * ------------------------------------------------------------------------------------------ */
+size_t givens_gemm_workspace_bytes(int32_t n, int64_t m);
+int givens_gemm_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
+                      float *Y, int64_t ldy, int transpose, const int32_t *perm, int32_t reflect_col, void *ws,
+                      size_t ws_bytes, void *stream);
+int givens_gemm_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *Y, int64_t ldy,
+                         const float *dY, int64_t lddy, float *dX, int64_t lddx, float *dtheta, int flags,
+                         const int32_t *perm, int32_t reflect_col, void *ws, size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

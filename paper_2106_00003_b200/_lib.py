@@ -22,7 +22,7 @@ EXPORTS = [
     "givens_build_U", "givens_backward", "givens_index_trace", "givens_u_supported", "givens_u_apply",
     "givens_u_build_U", "givens_u_backward", "givens_check_perm", "givens_schedule_ex", "givens_mask_from_dims_ex",
     "givens_apply_ex", "givens_build_U_ex", "givens_backward_ex", "givens_u_apply_ex", "givens_u_build_U_ex",
-    "givens_u_backward_ex",
+    "givens_u_backward_ex", "givens_gemm_workspace_bytes", "givens_gemm_apply", "givens_gemm_backward",
 ]
 
 
@@ -72,6 +72,12 @@ def lib():
         L.givens_u_build_U.argtypes = [I32, P, P, P, P, I64, P, SZ, P]
         L.givens_u_backward.restype = C
         L.givens_u_backward.argtypes = [I32, I64, P, P, P, P, I64, P, I64, P, I64, P, P, C, P, SZ, P]
+        L.givens_gemm_workspace_bytes.restype = SZ
+        L.givens_gemm_workspace_bytes.argtypes = [I32, I64]
+        L.givens_gemm_apply.restype = C
+        L.givens_gemm_apply.argtypes = [I32, I64, P, P, P, I64, P, I64, C, P, I32, P, SZ, P]
+        L.givens_gemm_backward.restype = C
+        L.givens_gemm_backward.argtypes = [I32, I64, P, P, P, I64, P, I64, P, I64, P, C, P, I32, P, SZ, P]
         L.givens_check_perm.restype = C
         L.givens_check_perm.argtypes = [I32, P]
         L.givens_schedule_ex.restype = C

@@ -134,7 +134,8 @@ struct RingArgs {
     const uint8_t *coef_ph;  // unitary: (p_t, q_t, p_b, q_b) phase factors per slot
     const uint8_t *coef_ab;  // unitary backward: (alpha, beta) dphi weights per slot
     const uint8_t *sfin;     // final sign per label
-    const int32_t *lrow;     // row of each label (start permutation; >= n for the odd-n bye)
+    const int32_t *lrow;     // row of each label under a start permutation (>= n: the odd-n bye);
+                             // NULL = identity (no dependent global loads at slab load/store)
     float *partial;   // BWD: per CTA, per reduction group, NW warp blocks (see red_geom)
     int64_t nslabs;
     int vec_ok;       // 1 if all row starts are 16-byte aligned for K-wide vector access
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             if (UP) { lt = row_sRm1(pt, ne); lb = row_sRm1(pb, ne); }
             else    { lt = row_s0(pt);       lb = row_s0(pb); }
             int rt = n, rb = n;  // rows; idle lanes hold zeros and never store
-            if (active) { rt = a.lrow[lt]; rb = a.lrow[lb]; }
+            if (active) { rt = a.lrow ? a.lrow[lt] : lt; rb = a.lrow ? a.lrow[lb] : lb; }
             V vt[KP], vb[KP];
             if constexpr (BM == M_BUILDU && UNI) {
 #pragma unroll
@@ -765,7 +766,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             if (UP) { lt = row_s0(pt); lb = row_s0(pb); }
             else    { lt = row_sRm1(pt, ne); lb = row_sRm1(pb, ne); }
             int rt = n, rb = n;
-            if (active) { rt = a.lrow[lt]; rb = a.lrow[lb]; }
+            if (active) { rt = a.lrow ? a.lrow[lt] : lt; rb = a.lrow ? a.lrow[lb] : lb; }
             V vt[KP], vb[KP];
 #pragma unroll
             for (int p = 0; p < KP; p++) {

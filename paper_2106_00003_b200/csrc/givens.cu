@@ -11,6 +11,7 @@
 //   k_dtheta_reduce            stage 2 of the dtheta reduction (fixed CTA order, no atomics);
 //   k_trace / k_trace_generic  index trace for the bit-exact schedule test.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdint.h>
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(32) k_generic(const GenArgs a) {
         const bool live = col < a.m;
         for (int i = 0; i < ne; i++) {  // i: label, row = lrow[i]
             float v = 0.f, d = 0.f;
-            const int row = a.lrow[i];
+            const int row = a.lrow ? a.lrow[i] : i;
             if (row < n && live) {
                 if (MODE == M_BUILDU) v = (col == row) ? 1.f : 0.f;
                 else v = a.X[(int64_t)row * a.ldx + col];
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(32) k_generic(const GenArgs a) {
         }
         if (live && !(GRAD && a.Y == nullptr)) {
             for (int i = 0; i < ne; i++) {
-                const int row = a.lrow[i];
+                const int row = a.lrow ? a.lrow[i] : i;
                 if (row >= n) continue;
                 float v = GRAD ? D[(int64_t)i * stride] : Z[(int64_t)i * stride];
                 if (!UP && a.sfin[i]) v = -v;
@@ -506,7 +507,7 @@ __global__ void __launch_bounds__(32) k_generic_u(const GenArgs a) {
         const bool live = col < mc;
         for (int i = 0; i < ne; i++) {  // i: label, row = lrow[i]
             float2 v = make_float2(0.f, 0.f), d = make_float2(0.f, 0.f);
-            const int row = a.lrow[i];
+            const int row = a.lrow ? a.lrow[i] : i;
             if (row < n && live) {
                 if (BM == M_BUILDU) v.x = (col == row) ? 1.f : 0.f;
                 else v = make_float2(a.X[(int64_t)row * a.ldx + 2 * col], a.X[(int64_t)row * a.ldx + 2 * col + 1]);
@@ -571,7 +572,7 @@ __global__ void __launch_bounds__(32) k_generic_u(const GenArgs a) {
         }
         if (live && !(GRAD && a.Y == nullptr)) {
             for (int i = 0; i < ne; i++) {
-                const int row = a.lrow[i];
+                const int row = a.lrow ? a.lrow[i] : i;
                 if (row >= n) continue;
                 float2 v = GRAD ? D[(int64_t)i * stride] : Z[(int64_t)i * stride];
                 if (!UP && a.sfin[i]) v = neg_v(v);
@@ -757,7 +758,8 @@ int vec_ok_for(int K, std::initializer_list<std::pair<const void *, int64_t>> ma
 }
 
 int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, const float *dY, int64_t lddy,
-                   float *Y, int64_t ldy, uint8_t *ws, const WsLayout &L, const Cfg &c, cudaStream_t st) {
+                   float *Y, int64_t ldy, uint8_t *ws, const WsLayout &L, const Cfg &c, cudaStream_t st,
+                   const int32_t *perm) {
     if (m == 0) return 0;
     int64_t grid = grid_for(c, mode, m);
     if (c.fast) {
@@ -765,7 +767,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
         ra.n = n; ra.ne = c.ne; ra.La = c.La;
         ra.m = m; ra.X = X; ra.ldx = ldx; ra.dY = dY; ra.lddy = lddy; ra.Y = Y; ra.ldy = ldy;
         ra.coef = ws + L.coef; ra.sfin = ws + L.sfin;
-        ra.lrow = reinterpret_cast<const int32_t *>(ws + L.lay);
+        ra.lrow = perm ? reinterpret_cast<const int32_t *>(ws + L.lay) : nullptr;
         ra.coef_ph = ws + L.coef_ph; ra.coef_ab = ws + L.coef_ab;
         ra.partial = reinterpret_cast<float *>(ws + L.partial);
         ra.nslabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
@@ -777,7 +779,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
     ga.n = n; ga.ne = c.ne; ga.S = c.S; ga.rowbytes = c.rowbytes; ga.m = m;
     ga.X = X; ga.ldx = ldx; ga.dY = dY; ga.lddy = lddy; ga.Y = Y; ga.ldy = ldy;
     ga.coef = ws + L.coef; ga.sfin = ws + L.sfin;
-    ga.lrow = reinterpret_cast<const int32_t *>(ws + L.lay);
+    ga.lrow = perm ? reinterpret_cast<const int32_t *>(ws + L.lay) : nullptr;
     ga.coef_ph = reinterpret_cast<const float4 *>(ws + L.coef_ph);
     ga.coef_ab = reinterpret_cast<const float2 *>(ws + L.coef_ab);
     ga.partial = reinterpret_cast<float *>(ws + L.partial);
@@ -891,7 +893,7 @@ int givens_u_apply_ex(int32_t n, int64_t m, const float *theta, const float *phi
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
     // a complex column is two interleaved real columns
     return run_apply_mode((adjoint ? M_TRANS : M_FWD) | M_UNI, n, 2 * m, X, 2 * ldx, nullptr, 0, Y, 2 * ldy, w, L,
-                          c, st);
+                          c, st, perm);
 }
 
 int givens_u_build_U_ex(int32_t n, const float *theta, const float *phi, const uint8_t *mask, float *U, int64_t ldu,
@@ -906,7 +908,7 @@ int givens_u_build_U_ex(int32_t n, const float *theta, const float *phi, const u
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
-    return run_apply_mode(M_BUILDU | M_UNI, n, 2 * (int64_t)n, nullptr, 0, nullptr, 0, U, 2 * ldu, w, L, c, st);
+    return run_apply_mode(M_BUILDU | M_UNI, n, 2 * (int64_t)n, nullptr, 0, nullptr, 0, U, 2 * ldu, w, L, c, st, perm);
 }
 
 int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *phi, const uint8_t *mask,
@@ -932,7 +934,7 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
         CUDA_TRY(cudaMemsetAsync(dphi, 0, (size_t)N * 4, st));
         return 0;
     }
-    if ((rc = run_apply_mode(M_BWD | M_UNI, n, 2 * m, Y, 2 * ldy, dY, 2 * lddy, dX, 2 * lddx, w, L, c, st))) return rc;
+    if ((rc = run_apply_mode(M_BWD | M_UNI, n, 2 * m, Y, 2 * ldy, dY, 2 * lddy, dX, 2 * lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD, 2 * m);
     int64_t tot = (int64_t)2 * c.S * c.S;
     k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
@@ -955,7 +957,7 @@ int givens_apply_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
-    return run_apply_mode(transpose ? M_TRANS : M_FWD, n, m, X, ldx, nullptr, 0, Y, ldy, w, L, c, st);
+    return run_apply_mode(transpose ? M_TRANS : M_FWD, n, m, X, ldx, nullptr, 0, Y, ldy, w, L, c, st, perm);
 }
 
 int givens_build_U_ex(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu,
@@ -971,7 +973,7 @@ int givens_build_U_ex(int32_t n, const float *theta, const uint8_t *mask, float 
     cudaStream_t st = (cudaStream_t)stream;
     uint8_t *w = (uint8_t *)ws;
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
-    return run_apply_mode(M_BUILDU, n, n, nullptr, 0, nullptr, 0, U, ldu, w, L, c, st);
+    return run_apply_mode(M_BUILDU, n, n, nullptr, 0, nullptr, 0, U, ldu, w, L, c, st, perm);
 }
 
 int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *Y, int64_t ldy,
@@ -995,7 +997,7 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
         CUDA_TRY(cudaMemsetAsync(dtheta, 0, (size_t)N * 4, st));
         return 0;
     }
-    if ((rc = run_apply_mode(M_BWD, n, m, Y, ldy, dY, lddy, dX, lddx, w, L, c, st))) return rc;
+    if ((rc = run_apply_mode(M_BWD, n, m, Y, ldy, dY, lddy, dX, lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD, m);
     int64_t tot = (int64_t)2 * c.S * c.S;
     k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
@@ -1063,3 +1065,5 @@ int givens_index_trace(int32_t n, int direction, int32_t *out_dev, void *stream)
 }
 
 }  // extern "C"
+
+#include "gemm_path.inc"

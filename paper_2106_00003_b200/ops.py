@@ -185,6 +185,51 @@ def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch
     return dtheta, dX
 
 
+# ---------------------------------------------------------------- GEMM path
+
+def gemm_workspace(n: int, m: int, device=None) -> torch.Tensor:
+    nb = int(lib().givens_gemm_workspace_bytes(n, m))
+    if nb == 0:
+        raise ValueError(f"bad GEMM workspace query n={n} m={m}")
+    return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
+
+
+def gemm_apply(theta, X, mask=None, transpose: bool = False, out=None, ws=None, layout: Layout | None = None):
+    """Y = U(theta) X via U-build (register ring) + a 3xTF32 tensor-core GEMM."""
+    n, m = X.shape
+    _check_matrix("X", X, n)
+    _check_theta(theta, mask, n)
+    Y = torch.empty_like(X) if out is None else out
+    _check_matrix("out", Y, n)
+    if ws is None:
+        ws = gemm_workspace(n, m, X.device)
+    check(lib().givens_gemm_apply(n, m, _ptr(theta), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y), Y.stride(0),
+                                  int(bool(transpose)), *_lay(layout, n, X.device), _ptr(ws), ws.numel(),
+                                  _stream(X.device)))
+    return Y
+
+
+def gemm_backward(theta, Y, dY, mask=None, want_dX: bool = True, ws=None, recompute: bool = True,
+                  dtheta=None, dX=None, layout: Layout | None = None):
+    """(dtheta, dX) via dX = U^T dY, Gamma = (dY Y^T) U (3xTF32 GEMMs) and Alg. 3 on Gamma."""
+    n, m = Y.shape
+    _check_matrix("Y", Y, n)
+    _check_matrix("dY", dY, n)
+    _check_theta(theta, mask, n)
+    if ws is None:
+        ws = gemm_workspace(n, m, Y.device)
+        recompute = True
+    if dtheta is None:
+        dtheta = torch.empty(num_angles(n), dtype=torch.float32, device=Y.device)
+    if want_dX and dX is None:
+        dX = torch.empty_like(dY)
+    check(lib().givens_gemm_backward(n, m, _ptr(theta), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY), dY.stride(0),
+                                     _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
+                                     FLAG_RECOMPUTE if recompute else 0, *_lay(layout, n, Y.device), _ptr(ws),
+                                     ws.numel(), _stream(Y.device)))
+    return dtheta, dX
+
+
 def index_trace(n: int, direction: int = 0, device=None) -> torch.Tensor:
     """Row ids the kernels pair per (block, slot), as (min, max): int32 [R][S][2] (device)."""
     ne = n_eff(n)
