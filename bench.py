@@ -248,6 +248,52 @@ def unitary_line(g, torch, synth, dev, peak_tflops, n=1024, m=32768, reps=5):
             "flops_per_complex_rotation_column": {"fwd": UFLOPS_FWD, "bwd": UFLOPS_BWD}}
 
 
+def _measured_peak(key, default):
+    """A number from the driver-written MEASURED_PEAKS.json, else the stated fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))[key])
+    except Exception:
+        return default
+
+
+def gemm_path_line(g, torch, theta, X, dY, n, m, ring_ms, tf32_peak, reps=10):
+    """SURVEY §8(f2) measured beside the ring: the same C3 fwd+bwd outputs (Y, dX, dtheta) from
+    U-build (ring) + 3xTF32 tensor-core GEMMs + Alg. 3 on Gamma (givens_gemm_apply/backward).
+    Device ms per step (mean of `reps` after warm-up, L2 flushed before each)."""
+    dev = X.device
+    ws = g.gemm_workspace(n, m, dev)
+    Y = torch.empty_like(X)
+    dX = torch.empty_like(X)
+    dth = torch.empty_like(theta)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        g.gemm_apply(theta, X, out=Y, ws=ws)
+        g.gemm_backward(theta, Y, dY, ws=ws, recompute=False, dtheta=dth, dX=dX)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tf = tb = 0.0
+    for _ in range(reps):
+        flush.fill_(1.0)
+        ev[0].record()
+        g.gemm_apply(theta, X, out=Y, ws=ws)
+        ev[1].record()
+        g.gemm_backward(theta, Y, dY, ws=ws, recompute=False, dtheta=dth, dX=dX)
+        ev[2].record()
+        torch.cuda.synchronize()
+        tf += ev[0].elapsed_time(ev[1])
+        tb += ev[1].elapsed_time(ev[2])
+    tf, tb = tf / reps, tb / reps
+    N = n * (n - 1) // 2
+    gemm_flops = 3 * (3 * 2.0 * n * n * m)  # Y = U X, dX = U^T dY, M = dY Y^T; three TF32 products each
+    return {"workload": f"C3 n={n}, m={m}: same outputs as the headline step (Y, dX, dtheta)",
+            "path": "build_U (ring) + 3xTF32 GEMMs (cuBLAS, K-chunked) + Alg. 3 on Gamma (ring replay, X = I)",
+            "fwd_ms": round(tf, 4), "bwd_ms": round(tb, 4), "ms_per_step": round(tf + tb, 4),
+            "equivalent_rotations_per_s": N * m / ((tf + tb) * 1e-3),
+            "speedup_vs_ring": round(ring_ms / (tf + tb), 3),
+            "tf32_gemm_flops_per_step": gemm_flops,
+            "tf32_peak_tflops": tf32_peak,
+            "note": "not the headline: the headline is the SURVEY 8(a) ring path; this is the 8(f2) row"}
+
+
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
@@ -402,7 +448,7 @@ def main():
                                        "(max boost; DESIGN.md §5)",
                          "flops_per_rotation_column": FLOPS_BWD, "ms_per_launch": ms_bwd},
             "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd,
-            "gpu_launches": 6 * args.steps,
+            "gpu_launches": 7 * args.steps,
             "clocks": clk,
         }
         if e2e:
@@ -411,6 +457,8 @@ def main():
             out["ubuild_ms_vs_n"] = ubuild
         if world == 1 and not args.no_ubuild:
             out["unitary"] = unitary_line(g, torch, synth, dev, peak)
+            bf16 = _measured_peak("bf16_tflops", 2250.0)
+            out["f2_gemm_path"] = gemm_path_line(g, torch, theta, X, dY, n, m, ms_step, bf16 / 2)
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out), flush=True)

@@ -67,7 +67,9 @@ __host__ __device__ constexpr int ring_warps(int mode) { return (mode & 3) == 3 
 
 // base modes; M_UNI marks the unitary U(n) variant (Appendix A): complex columns stored as
 // interleaved (re, im) pairs, i.e. two real columns per complex column
-enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4 };
+// M_IDLE (launch-time only) selects the instantiation with idle lanes (La < L, runtime La); without
+// it La == L is a compile-time constant (fewer registers and address computations)
+enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8 };
 
 __host__ __device__ constexpr int kcols(int W, int mode) {
     // real columns per thread, so that the column state is ~128 registers (2 W K forward, 4 W K
@@ -348,7 +350,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     constexpr int LW = G::LW, H = G::H, LC = G::LC, SPS = G::SPS, NSTAGE = G::NSTAGE;
     // active geometry: L lanes are instantiated, the last warp of a group may leave lanes idle
     // (S = W * La with La in (L - 32, L]); buffers are sized for the instantiated maximum
-    const int La = (H == 1 && LC > 1) ? L : a.La;
+    constexpr bool IDLE = (MODE & M_IDLE) != 0 && !(H == 1 && LC > 1);
+    const int La = IDLE ? a.La : L;
     const int S = W * La, STEPS = 2 * S;
     const int rowb = S * 8;                       // bytes per (t, s) table row
     const uint32_t stage_bytes = (uint32_t)(SPS * S * G::RB);

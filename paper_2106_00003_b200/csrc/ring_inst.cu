@@ -23,8 +23,24 @@ static cudaError_t launch_wlm(const RingArgs &ra, int64_t grid, cudaStream_t st)
     return cudaGetLastError();
 }
 
+// configurations that also serve n with idle lanes (S = W * La, La < L; see make_cfg)
+#define GK_IDLE_CAPABLE ((RING_W == 16 || RING_W == 8) && (RING_L == 32 || RING_L == 64 || RING_L == 128))
+
 cudaError_t GK_CAT(ring_launch_, RING_W, RING_L)(int mode, const RingArgs &ra, int64_t grid, cudaStream_t st) {
+    if (ra.La != RING_L) mode |= M_IDLE;
     switch (mode) {
+#if GK_IDLE_CAPABLE
+        case M_FWD | M_IDLE: return launch_wlm<RING_W, RING_L, M_FWD | M_IDLE>(ra, grid, st);
+        case M_BUILDU | M_IDLE: return launch_wlm<RING_W, RING_L, M_BUILDU | M_IDLE>(ra, grid, st);
+        case M_TRANS | M_IDLE: return launch_wlm<RING_W, RING_L, M_TRANS | M_IDLE>(ra, grid, st);
+        case M_BWD | M_IDLE: return launch_wlm<RING_W, RING_L, M_BWD | M_IDLE>(ra, grid, st);
+#if RING_W * RING_L <= 1024
+        case M_FWD | M_UNI | M_IDLE: return launch_wlm<RING_W, RING_L, M_FWD | M_UNI | M_IDLE>(ra, grid, st);
+        case M_BUILDU | M_UNI | M_IDLE: return launch_wlm<RING_W, RING_L, M_BUILDU | M_UNI | M_IDLE>(ra, grid, st);
+        case M_TRANS | M_UNI | M_IDLE: return launch_wlm<RING_W, RING_L, M_TRANS | M_UNI | M_IDLE>(ra, grid, st);
+        case M_BWD | M_UNI | M_IDLE: return launch_wlm<RING_W, RING_L, M_BWD | M_UNI | M_IDLE>(ra, grid, st);
+#endif
+#endif
         case M_FWD: return launch_wlm<RING_W, RING_L, M_FWD>(ra, grid, st);
         case M_BUILDU: return launch_wlm<RING_W, RING_L, M_BUILDU>(ra, grid, st);
         case M_TRANS: return launch_wlm<RING_W, RING_L, M_TRANS>(ra, grid, st);
