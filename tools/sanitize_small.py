@@ -18,3 +18,25 @@ for n, m in sizes:
     g.index_trace(n, 0); g.index_trace(n, 1)
     torch.cuda.synchronize()
     print("ok", n, m, flush=True)
+# unitary (ring, idle-lane ring, generic), layout options, GEMM path
+for n, m in [(7, 5), (48, 9), (64, 6), (256, 12), (100, 4)]:
+    if len(sys.argv) > 1 and n > int(sys.argv[1]):
+        continue
+    N = n * (n - 1) // 2
+    th = torch.from_numpy(synth.theta(N, seed=1)).cuda()
+    ph = torch.from_numpy(synth.theta(N, seed=2)).cuda()
+    X = torch.complex(torch.from_numpy(synth.normal_matrix(n, m, 1, 2)), torch.from_numpy(synth.normal_matrix(n, m, 2, 2))).cuda()
+    G = torch.complex(torch.from_numpy(synth.normal_matrix(n, m, 1, 3)), torch.from_numpy(synth.normal_matrix(n, m, 2, 3))).cuda()
+    lay = g.Layout(n, perm=np.random.default_rng(n).permutation(n + n % 2), reflect_col=n // 2)
+    Y = g.u_apply(th, ph, X, layout=lay)
+    g.u_apply(th, ph, X, adjoint=True)
+    g.u_backward(th, ph, Y, G, layout=lay)
+    g.u_build_U(th, ph, n)
+    Xr = X.real.contiguous()
+    Yr = g.apply(th, Xr, layout=lay)
+    g.backward(th, Yr, G.real.contiguous(), layout=lay)
+    ws = g.gemm_workspace(n, m)
+    Yg = g.gemm_apply(th, Xr, ws=ws, layout=lay)
+    g.gemm_backward(th, Yg, G.real.contiguous(), ws=ws, recompute=False, layout=lay)
+    torch.cuda.synchronize()
+    print("ok-u/layout/gemm", n, m, flush=True)
