@@ -209,6 +209,36 @@ def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 409
 UFLOPS_FWD, UFLOPS_BWD = 18, 64
 
 
+def small_config_line(g, torch, synth, dev, n=256, m=4096, reps=20):
+    """BASELINE config C2 (n=256, m=4096, 1 GPU): device ms of apply + backward (dX, dtheta), mean of
+    `reps` after warm-up, L2 flushed before each; latency-bound (28 columns per SM)."""
+    N = n * (n - 1) // 2
+    th = torch.from_numpy(synth.theta(N, seed=SEED)).to(dev)
+    X = torch.from_numpy(synth.normal_matrix(n, m, SEED, synth.TID_X)).to(dev)
+    dY = torch.from_numpy(synth.normal_matrix(n, m, SEED, synth.TID_DY)).to(dev)
+    ws = g.workspace(g.OP_BACKWARD, n, m, dev)
+    Y, dX, dth = torch.empty_like(X), torch.empty_like(X), torch.empty(N, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        g.apply(th, X, out=Y, ws=ws)
+        g.backward(th, Y, dY, ws=ws, recompute=False, dtheta=dth, dX=dX)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tf = tb = 0.0
+    for _ in range(reps):
+        flush.fill_(1.0)
+        ev[0].record()
+        g.apply(th, X, out=Y, ws=ws)
+        ev[1].record()
+        g.backward(th, Y, dY, ws=ws, recompute=False, dtheta=dth, dX=dX)
+        ev[2].record()
+        torch.cuda.synchronize()
+        tf += ev[0].elapsed_time(ev[1])
+        tb += ev[1].elapsed_time(ev[2])
+    tf, tb = tf / reps, tb / reps
+    return {"workload": f"C2 n={n}, m={m}: apply + backward (dX, dtheta)", "fwd_ms": round(tf, 4),
+            "bwd_ms": round(tb, 4), "rotations_per_s": N * m / ((tf + tb) * 1e-3)}
+
+
 def unitary_line(g, torch, synth, dev, peak_tflops, n=1024, m=32768, reps=5):
     """the unitary U(n) path (Appendix A) at n = 1024 on m complex columns (the same
     2m = 65536 real columns as C3): device ms of u_apply and u_backward, mean of `reps` after
@@ -456,6 +486,7 @@ def main():
         if ubuild:
             out["ubuild_ms_vs_n"] = ubuild
         if world == 1 and not args.no_ubuild:
+            out["c2"] = small_config_line(g, torch, synth, dev)
             out["unitary"] = unitary_line(g, torch, synth, dev, peak)
             bf16 = _measured_peak("bf16_tflops", 2250.0)
             out["f2_gemm_path"] = gemm_path_line(g, torch, theta, X, dY, n, m, ms_step, bf16 / 2)

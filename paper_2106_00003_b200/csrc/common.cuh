@@ -63,18 +63,24 @@ constexpr int kNW = GK_BWD_WARPS;  // warps per CTA of the backward ring kernel
 #define GK_FWD_WARPS 8
 #endif
 constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose ring kernels
-__host__ __device__ constexpr int ring_warps(int mode) { return (mode & 3) == 3 ? kNW : kNWF; }
-
 // base modes; M_UNI marks the unitary U(n) variant (Appendix A): complex columns stored as
 // interleaved (re, im) pairs, i.e. two real columns per complex column
 // M_IDLE (launch-time only) selects the instantiation with idle lanes (La < L, runtime La); without
 // it La == L is a compile-time constant (fewer registers and address computations)
-enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8 };
+// M_NARROW (launch-time only): 4-warp CTAs with at most 2 columns per thread, for batches too
+// small to give every SM a slab at the normal width (U-build and Alg. 3 at n <= 2048, C2)
+enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16 };
+constexpr int kNWN = 4;  // warps per CTA of the narrow variant
+
+__host__ __device__ constexpr int ring_warps(int mode) {
+    return (mode & M_NARROW) ? kNWN : ((mode & 3) == 3 ? kNW : kNWF);
+}
 
 __host__ __device__ constexpr int kcols(int W, int mode) {
     // real columns per thread, so that the column state is ~128 registers (2 W K forward, 4 W K
     // backward); two packed fp32 columns per FFMA2 (one complex column in the unitary variant)
-    return ((mode & 3) == M_BWD) ? (32 / W > 8 ? 8 : 32 / W) : (64 / W > 8 ? 8 : 64 / W);
+    const int k = ((mode & 3) == M_BWD) ? (32 / W > 8 ? 8 : 32 / W) : (64 / W > 8 ? 8 : 64 / W);
+    return ((mode & M_NARROW) && k > 2) ? 2 : k;
 }
 
 // ------------------------------------------------------------------ PTX helpers
@@ -264,10 +270,10 @@ __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.p
 struct RedGeom {
     int LW, H, NCHW, NSUM, OUTCH, RG, NW;
 };
-__host__ __device__ constexpr RedGeom red_geom(int W, int L, int vals = 1) {
-    int LW = L < 32 ? L : 32, H = L / LW, NCHW = (W / 4) * LW * vals, NSUM = kNW / H;
-    int RG = (NCHW >= 256 || (H > 1 && NCHW >= 128) || kNW > 8 || vals > 1) ? 2 : 4;
-    return RedGeom{LW, H, NCHW, NSUM, (NCHW + NSUM - 1) / NSUM, RG, kNW};
+__host__ __device__ constexpr RedGeom red_geom(int W, int L, int vals = 1, int NW = kNW) {
+    int LW = L < 32 ? L : 32, H = L / LW, NCHW = (W / 4) * LW * vals, NSUM = NW / H;
+    int RG = (NCHW >= 256 || (H > 1 && NCHW >= 128) || NW > 8 || vals > 1) ? 2 : 4;
+    return RedGeom{LW, H, NCHW, NSUM, (NCHW + NSUM - 1) / NSUM, RG, NW};
 }
 
 // Compile-time geometry of one ring configuration: W slots per lane, L lanes per column group
@@ -303,7 +309,7 @@ struct RingGeom {
     // backward sums (dtheta, and dphi in the unitary variant): per-warp ring of NG groups of RG
     // steps, reduced one group later
     static constexpr int VALS = UNI ? 2 : 1;
-    static constexpr int RG = red_geom(W, L, VALS).RG;  // steps per reduction group
+    static constexpr int RG = red_geom(W, L, VALS, NW).RG;  // steps per reduction group
     static constexpr int NG = 2;                    // groups in flight
     static constexpr int D = RG * NG;               // ring depth in steps
     static constexpr int NCHW1 = (W / 4) * LW;      // dtheta chunks held by one warp

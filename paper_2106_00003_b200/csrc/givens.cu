@@ -151,7 +151,20 @@ int64_t cols_per_slab(const Cfg &c, int mode) {
     return (int64_t)ring_warps(mode) * LC / H * kcols(c.W, mode);
 }
 
-int64_t grid_for(const Cfg &c, int mode, int64_t m) {
+// the launch mode for m columns: the narrow variant when the normal width leaves SMs without a
+// slab (real ring kernels with single-warp column groups only: with H > 1 warps per group the
+// per-step exchange barrier would be amortised over half the columns -- measured 2x slower)
+int launch_mode(const Cfg &c, int mode, int64_t m) {
+    if (!c.fast || (mode & M_UNI) || (mode & M_NARROW)) return mode;
+    const int H = c.L < 32 ? 1 : c.L / 32;
+    if (H > 1) return mode;
+    const int64_t slabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
+    const int64_t slabs_n = (m + cols_per_slab(c, mode | M_NARROW) - 1) / cols_per_slab(c, mode | M_NARROW);
+    return (slabs < dev_sms() && slabs_n > slabs) ? (mode | M_NARROW) : mode;
+}
+
+int64_t grid_for(const Cfg &c, int mode0, int64_t m) {
+    const int mode = launch_mode(c, mode0, m);
     int64_t slabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
     int64_t per_sm = c.fast ? 1 : 8;
     int64_t g = std::min<int64_t>(slabs, (int64_t)dev_sms() * per_sm);
@@ -182,10 +195,10 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     L.lay = off; off = al256(off + (size_t)(c.ne + 2) * 4);
     L.partial = off;
     if (base == GIVENS_OP_BACKWARD) {
-        int64_t g = grid_for(c, M_BWD, mr);
+        int64_t g = grid_for(c, M_BWD | (uni ? M_UNI : 0), mr);
         size_t per_step = (size_t)c.S * 4 * (uni ? 2 : 1);  // generic kernel: natural order, [vals][2S][S]
         if (c.fast) {
-            const RedGeom rg = red_geom(c.W, c.L, uni ? 2 : 1);
+            const RedGeom rg = red_geom(c.W, c.L, uni ? 2 : 1, ring_warps(launch_mode(c, M_BWD | (uni ? M_UNI : 0), mr)));
             per_step = (size_t)rg.NW * rg.OUTCH * 16;  // >= S floats (padded when chunks don't split evenly)
         }
         off = al256(off + (size_t)g * 2 * c.S * per_step);
@@ -353,7 +366,7 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
 // ------------------------------------------------------------------ stage-2 dtheta reduction
 // dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in fixed CTA order (PAPER.md:768-781
 // "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0.
-__global__ void k_dtheta_reduce(int S, int W, int L, int G, int ring, int vals, const float *__restrict__ partial,
+__global__ void k_dtheta_reduce(int S, int W, int L, int NW, int G, int ring, int vals, const float *__restrict__ partial,
                                 const int32_t *__restrict__ amap, float *__restrict__ dtheta, float *__restrict__ dphi) {
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int rows = 2 * S;
@@ -373,7 +386,7 @@ __global__ void k_dtheta_reduce(int S, int W, int L, int G, int ring, int vals, 
             // ring kernel layout: per CTA, per group of RG steps, NW warp blocks of RG x OUTCH float4;
             // slot k (lane t = k / W of the group, slot q = k % W) is chunk ci = v*NCHW1 + (q/4)*LW + t%LW
             // of the warp slice t/LW (v = 0: dtheta, 1: dphi), reduced by the warp c*H + slice owning ci
-            const RedGeom rg = red_geom(W, L, vals);
+            const RedGeom rg = red_geom(W, L, vals, NW);
             const int nchw1 = rg.NCHW / vals;
             int t = k / W, q = k % W, hs = t / rg.LW, tl = t % rg.LW;
             int ci = v * nchw1 + (q >> 2) * rg.LW + tl;
@@ -762,6 +775,7 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
                    const int32_t *perm) {
     if (m == 0) return 0;
     int64_t grid = grid_for(c, mode, m);
+    if (c.fast) mode = launch_mode(c, mode, m);
     if (c.fast) {
         RingArgs ra;
         ra.n = n; ra.ne = c.ne; ra.La = c.La;
@@ -935,10 +949,11 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
         return 0;
     }
     if ((rc = run_apply_mode(M_BWD | M_UNI, n, 2 * m, Y, 2 * ldy, dY, 2 * lddy, dX, 2 * lddx, w, L, c, st, perm))) return rc;
-    int64_t G = grid_for(c, M_BWD, 2 * m);
+    int64_t G = grid_for(c, M_BWD | M_UNI, 2 * m);
     int64_t tot = (int64_t)2 * c.S * c.S;
     k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, c.fast, 2, reinterpret_cast<const float *>(w + L.partial),
+        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD | M_UNI, 2 * m)), (int)G, c.fast, 2,
+        reinterpret_cast<const float *>(w + L.partial),
         reinterpret_cast<const int32_t *>(w + L.amap), dtheta, dphi);
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -1001,7 +1016,8 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
     int64_t G = grid_for(c, M_BWD, m);
     int64_t tot = (int64_t)2 * c.S * c.S;
     k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
-        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, (int)G, c.fast, 1, reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
+        c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD, m)), (int)G, c.fast, 1,
+        reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
         dtheta, nullptr);
     CUDA_TRY(cudaGetLastError());
     return 0;

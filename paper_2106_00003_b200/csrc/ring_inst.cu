@@ -29,6 +29,20 @@ static cudaError_t launch_wlm(const RingArgs &ra, int64_t grid, cudaStream_t st)
 cudaError_t GK_CAT(ring_launch_, RING_W, RING_L)(int mode, const RingArgs &ra, int64_t grid, cudaStream_t st) {
     if (ra.La != RING_L) mode |= M_IDLE;
     switch (mode) {
+#if RING_L <= 32  // narrow (4-warp, <= 2 columns per thread) real-valued variants for small batches;
+                  // single-warp column groups only (see launch_mode in givens.cu)
+        case M_FWD | M_NARROW: return launch_wlm<RING_W, RING_L, M_FWD | M_NARROW>(ra, grid, st);
+        case M_BUILDU | M_NARROW: return launch_wlm<RING_W, RING_L, M_BUILDU | M_NARROW>(ra, grid, st);
+        case M_TRANS | M_NARROW: return launch_wlm<RING_W, RING_L, M_TRANS | M_NARROW>(ra, grid, st);
+        case M_BWD | M_NARROW: return launch_wlm<RING_W, RING_L, M_BWD | M_NARROW>(ra, grid, st);
+#if GK_IDLE_CAPABLE
+        case M_FWD | M_NARROW | M_IDLE: return launch_wlm<RING_W, RING_L, M_FWD | M_NARROW | M_IDLE>(ra, grid, st);
+        case M_BUILDU | M_NARROW | M_IDLE:
+            return launch_wlm<RING_W, RING_L, M_BUILDU | M_NARROW | M_IDLE>(ra, grid, st);
+        case M_TRANS | M_NARROW | M_IDLE: return launch_wlm<RING_W, RING_L, M_TRANS | M_NARROW | M_IDLE>(ra, grid, st);
+        case M_BWD | M_NARROW | M_IDLE: return launch_wlm<RING_W, RING_L, M_BWD | M_NARROW | M_IDLE>(ra, grid, st);
+#endif
+#endif
 #if GK_IDLE_CAPABLE
         case M_FWD | M_IDLE: return launch_wlm<RING_W, RING_L, M_FWD | M_IDLE>(ra, grid, st);
         case M_BUILDU | M_IDLE: return launch_wlm<RING_W, RING_L, M_BUILDU | M_IDLE>(ra, grid, st);
