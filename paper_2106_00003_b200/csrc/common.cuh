@@ -293,18 +293,20 @@ struct RingGeom {
     static constexpr int KP = (K + 1) / 2;          // packed register pairs per slot
     // table bytes per slot staged per block: (t, s) 8 B; unitary adds the phases (16 B) and, in
     // the backward, the dphi weights (alpha, beta) (8 B)
-    static constexpr int RB = 8 + (UNI ? 16 : 0) + ((UNI && GRAD) ? 8 : 0);
+    // (forward / adjoint apply: the phases as two FFMA2-ready pairs per side, 32 B)
+    static constexpr int PHB = UNI ? (GRAD ? 16 : 32) : 0;  // phase bytes per slot
+    static constexpr int RB = 8 + PHB + ((UNI && GRAD) ? 8 : 0);
     // table rows per TMA stage: a power of two dividing W/2, stages of <= 32 KB forward and
     // <= 16 KB next to the dtheta ring
     static constexpr int sps_pick() {
         int v = W / 2;
-        while (v > 1 && v * S * RB > (GRAD ? 16384 : 32768)) v /= 2;
+        while (v > 1 && v * S * RB > (GRAD ? 16384 : (UNI ? 40960 : 32768))) v /= 2;
         return v;
     }
     static constexpr int SPS = sps_pick();
     static constexpr int STAGEB = SPS * S * RB;
     // stages in flight: 64 KB of table buffers next to the backward's dtheta ring, 96 KB otherwise
-    static constexpr int NSTAGE_ = (GRAD ? 65536 : 98304) / STAGEB;
+    static constexpr int NSTAGE_ = (GRAD ? 65536 : (UNI ? 163840 : 98304)) / STAGEB;
     static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
     // backward sums (dtheta, and dphi in the unitary variant): per-warp ring of NG groups of RG
     // steps, reduced one group later
@@ -333,6 +335,13 @@ __device__ __forceinline__ float2 cmulc(float2 z, float p, float q) {
 }
 __device__ __forceinline__ float cmul(float z, float, float) { return z; }
 __device__ __forceinline__ float cmulc(float z, float, float) { return z; }
+// the same with the factor pre-arranged as (a, b, c, d): z -> (z.x a + z.y c, z.x b + z.y d), i.e.
+// e = (p, q, -q, p) multiplies by p + i q and (p, -q, q, p) by its conjugate -- one FMUL2 + one
+// FFMA2 on register pairs as loaded
+__device__ __forceinline__ float2 cmul4(float2 z, float4 e) {
+    return __ffma2_rn(make_float2(z.y, z.y), make_float2(e.z, e.w), __fmul2_rn(make_float2(z.x, z.x), make_float2(e.x, e.y)));
+}
+__device__ __forceinline__ float cmul4(float z, float4) { return z; }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -430,7 +439,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         mbar_expect_tx(&full[b], stage_bytes);
         bulk_g2s(dst, a.coef + (int64_t)rho0 * rowb, (uint32_t)(SPS * rowb), &full[b]);
         if constexpr (UNI) {
-            bulk_g2s(dst + SPS * rowb, a.coef_ph + (int64_t)rho0 * 2 * rowb, (uint32_t)(SPS * 2 * rowb), &full[b]);
+            constexpr int PR = G::PHB / 8;  // phase bytes per slot in units of the (t, s) row
+            bulk_g2s(dst + SPS * rowb, a.coef_ph + (int64_t)rho0 * PR * rowb, (uint32_t)(SPS * PR * rowb), &full[b]);
             if constexpr (GRAD)
                 bulk_g2s(dst + SPS * 3 * rowb, a.coef_ab + (int64_t)rho0 * rowb, (uint32_t)(SPS * rowb), &full[b]);
         }
@@ -562,7 +572,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 const int srow = UP ? su : (SPS - 1 - su);
                 const uint8_t *sbase = stagebuf + (gst % NSTAGE) * G::STAGEB;
                 const float4 *row4 = reinterpret_cast<const float4 *>(sbase + srow * rowb);
-                const float4 *ph4 = reinterpret_cast<const float4 *>(sbase + SPS * rowb + srow * 2 * rowb);
+                const float4 *ph4 = reinterpret_cast<const float4 *>(sbase + SPS * rowb + srow * (G::PHB / 8) * rowb);
                 const float4 *ab4 = reinterpret_cast<const float4 *>(sbase + SPS * 3 * rowb + srow * rowb);
                 constexpr int r = uu % RG;
                 int bi = 0;
@@ -586,8 +596,13 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     for (int hh = 0; hh < 2; hh++) {
                         const int q = 2 * pp + hh;
                         const float tq = hh ? cf.z : cf.x, sq = hh ? cf.w : cf.y;
-                        float4 ph = make_float4(1.f, 0.f, 1.f, 0.f);
-                        if constexpr (UNI) ph = ph4[q * La + tc];  // (p_t, q_t, p_b, q_b)
+                        float4 ph = make_float4(1.f, 0.f, 1.f, 0.f), pha = ph, phb = ph;
+                        if constexpr (UNI && GRAD) ph = ph4[q * La + tc];  // (p_t, q_t, p_b, q_b)
+                        if constexpr (UNI && !GRAD) {
+                            // (p, q, -q, p) forward / (p, -q, q, p) adjoint, top then bottom
+                            pha = ph4[(2 * q) * La + tc];
+                            phb = ph4[(2 * q + 1) * La + tc];
+                        }
                         if constexpr (GRAD) {
                             // dtheta contribution before this block's inverse rotation:
                             // dz_bottom * z_top - dz_top * z_bottom (Q_e structure, PAPER.md:515-521;
@@ -616,18 +631,19 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                             if (UP) {
                                 if constexpr (GRAD) rot_inv2(ZT[p][q], ZB[p][q], DT[p][q], DB[p][q], tq, sq);
                                 else rot_inv(ZT[p][q], ZB[p][q], tq, sq);
-                                if constexpr (UNI) {  // G^dagger = diag(conj phases) R^T
+                                if constexpr (UNI && GRAD) {  // G^dagger = diag(conj phases) R^T
                                     ZT[p][q] = cmulc(ZT[p][q], ph.x, ph.y);
                                     ZB[p][q] = cmulc(ZB[p][q], ph.z, ph.w);
-                                    if constexpr (GRAD) {
-                                        DT[p][q] = cmulc(DT[p][q], ph.x, ph.y);
-                                        DB[p][q] = cmulc(DB[p][q], ph.z, ph.w);
-                                    }
+                                    DT[p][q] = cmulc(DT[p][q], ph.x, ph.y);
+                                    DB[p][q] = cmulc(DB[p][q], ph.z, ph.w);
+                                } else if constexpr (UNI) {
+                                    ZT[p][q] = cmul4(ZT[p][q], pha);
+                                    ZB[p][q] = cmul4(ZB[p][q], phb);
                                 }
                             } else {
                                 if constexpr (UNI) {  // G = R diag(phases): phase first
-                                    ZT[p][q] = cmul(ZT[p][q], ph.x, ph.y);
-                                    ZB[p][q] = cmul(ZB[p][q], ph.z, ph.w);
+                                    ZT[p][q] = cmul4(ZT[p][q], pha);
+                                    ZB[p][q] = cmul4(ZB[p][q], phb);
                                 }
                                 rot_fwd(ZT[p][q], ZB[p][q], tq, sq);
                             }

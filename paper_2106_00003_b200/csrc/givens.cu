@@ -172,7 +172,7 @@ int64_t grid_for(const Cfg &c, int mode0, int64_t m) {
 }
 
 struct WsLayout {
-    size_t coef, coef_ph, coef_ab, amap, flip, sig, sfin, lay, partial, scratch, total;
+    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, lay, partial, scratch, total;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
@@ -187,6 +187,8 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     const size_t rows = (size_t)(2 * c.S + 1);
     L.coef = off; off = al256(off + rows * c.rowbytes);
     L.coef_ph = off; if (uni) off = al256(off + rows * c.S * 16);
+    L.coef_pf = off; if (uni) off = al256(off + rows * c.S * 32);  // forward pairs (p, q, -q, p)
+    L.coef_pt = off; if (uni) off = al256(off + rows * c.S * 32);  // adjoint pairs (p, -q, q, p)
     L.coef_ab = off; if (uni) off = al256(off + rows * c.S * 8);
     L.amap = off; off = al256(off + rows * c.S * 4);
     L.flip = off; off = al256(off + (size_t)c.R * c.S);
@@ -333,7 +335,8 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
 // = cos(th_r) z_i + sigma_i sigma_j sin(th_r) z_j, th_r the pi-reduced angle.
 __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ theta, const float *__restrict__ phi,
                          const uint8_t *__restrict__ mask, const uint8_t *__restrict__ sig,
-                         const int32_t *__restrict__ lay, float4 *__restrict__ ph, float2 *__restrict__ ab) {
+                         const int32_t *__restrict__ lay, float4 *__restrict__ ph, float4 *__restrict__ pf,
+                         float4 *__restrict__ pt, float2 *__restrict__ ab) {
     int S = ne / 2, R = ne - 1;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)(R + 2) * S) return;
@@ -346,6 +349,8 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
     if (rho == 0 || rho == R + 1) {
         phr[pos_ph] = make_float4(1.f, 0.f, 1.f, 0.f);
         abr[pos_ab] = make_float2(0.f, 0.f);
+        const int64_t pp0 = (int64_t)rho * 2 * S + (2 * q) * L + t, pp1 = pp0 + L;
+        pf[pp0] = pf[pp1] = pt[pp0] = pt[pp1] = make_float4(1.f, 0.f, 0.f, 1.f);
         return;
     }
     int r = rho - 1;
@@ -358,6 +363,15 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
     float pc = (float)cos(pv), ps = (float)sin(pv);
     bool top_is_i = lay[a] < lay[b];
     phr[pos_ph] = top_is_i ? make_float4(pc, ps, 1.f, 0.f) : make_float4(1.f, 0.f, pc, ps);
+    {   // FFMA2-ready pairs per side, top then bottom: (p, q, -q, p) forward, (p, -q, q, p) adjoint
+        const int64_t pp0 = (int64_t)rho * 2 * S + (2 * q) * L + t, pp1 = pp0 + L;
+        const float4 one = make_float4(1.f, 0.f, 0.f, 1.f);
+        const float4 f = make_float4(pc, ps, -ps, pc), c = make_float4(pc, -ps, ps, pc);
+        pf[pp0] = top_is_i ? f : one;
+        pf[pp1] = top_is_i ? one : f;
+        pt[pp0] = top_is_i ? c : one;
+        pt[pp1] = top_is_i ? one : c;
+    }
     double cr = cos(thr), sr = sin(thr);
     if (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) sr = -sr;
     abr[pos_ab] = top_is_i ? make_float2((float)cr, (float)sr) : make_float2((float)sr, (float)cr);
@@ -744,6 +758,8 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
     if (phi) {
         k_coef_u<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, theta, phi, mask, ws + L.sig, lay,
                                                                 reinterpret_cast<float4 *>(ws + L.coef_ph),
+                                                                reinterpret_cast<float4 *>(ws + L.coef_pf),
+                                                                reinterpret_cast<float4 *>(ws + L.coef_pt),
                                                                 reinterpret_cast<float2 *>(ws + L.coef_ab));
         CUDA_TRY(cudaGetLastError());
     }
@@ -782,7 +798,10 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
         ra.m = m; ra.X = X; ra.ldx = ldx; ra.dY = dY; ra.lddy = lddy; ra.Y = Y; ra.ldy = ldy;
         ra.coef = ws + L.coef; ra.sfin = ws + L.sfin;
         ra.lrow = perm ? reinterpret_cast<const int32_t *>(ws + L.lay) : nullptr;
-        ra.coef_ph = ws + L.coef_ph; ra.coef_ab = ws + L.coef_ab;
+        // unitary phases: FFMA2-ready pairs for the forward / adjoint apply, the compact form for the
+        // backward (which also needs the (alpha, beta) weights)
+        ra.coef_ph = ws + ((mode & 3) == M_BWD ? L.coef_ph : ((mode & 3) == M_TRANS ? L.coef_pt : L.coef_pf));
+        ra.coef_ab = ws + L.coef_ab;
         ra.partial = reinterpret_cast<float *>(ws + L.partial);
         ra.nslabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
         int K = kcols(c.W, mode);
