@@ -30,6 +30,7 @@
  * stream   cudaStream_t (as void*), NULL = legacy default stream. Every call is
  *          stream-ordered and asynchronous: it enqueues kernels and returns; results are
  *          visible after the stream is synchronised. No call allocates device memory.
+ * empty    m = 0 is valid: X, Y, dY, dX may then be NULL; dtheta (dphi) is written as zeros.
  * errors   0 on success; negative givens_status_t otherwise, with a thread-local message
  *          from givens_last_error(). Parameter errors are detected before anything is
  *          enqueued. Asynchronous CUDA faults surface at the next synchronising call.

@@ -916,7 +916,7 @@ int givens_u_apply_ex(int32_t n, int64_t m, const float *theta, const float *phi
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_U_APPLY);
     if (rc) return rc;
     if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
-    if (!theta || !phi || !X || !Y) return fail(GIVENS_EINVAL, "theta, phi, X and Y must be non-NULL");
+    if (!theta || !phi || (m > 0 && (!X || !Y))) return fail(GIVENS_EINVAL, "theta, phi, X and Y must be non-NULL");
     if (ldx < m || ldy < m) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (X == Y && ldx != ldy) return fail(GIVENS_EINVAL, "in-place apply needs ldx == ldy");
     Cfg c = make_cfg_u(n);
@@ -950,7 +950,7 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_U_BACKWARD);
     if (rc) return rc;
     if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
-    if (!theta || !phi || !Y || !dY || !dtheta || !dphi)
+    if (!theta || !phi || !dtheta || !dphi || (m > 0 && (!Y || !dY)))
         return fail(GIVENS_EINVAL, "theta, phi, Y, dY, dtheta and dphi must be non-NULL");
     if (ldy < m || lddy < m || (dX && lddx < m)) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (dX && dX == dY && lddx != lddy) return fail(GIVENS_EINVAL, "in-place dX needs lddx == lddy");
@@ -983,7 +983,7 @@ int givens_apply_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_APPLY);
     if (rc) return rc;
     if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
-    if (!theta || !X || !Y) return fail(GIVENS_EINVAL, "theta, X and Y must be non-NULL");
+    if (!theta || (m > 0 && (!X || !Y))) return fail(GIVENS_EINVAL, "theta, X and Y must be non-NULL");
     if (ldx < m || ldy < m) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (X == Y && ldx != ldy) return fail(GIVENS_EINVAL, "in-place apply needs ldx == ldy");
     Cfg c = make_cfg(n);
@@ -1016,7 +1016,7 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
     int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_BACKWARD);
     if (rc) return rc;
     if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
-    if (!theta || !Y || !dY || !dtheta) return fail(GIVENS_EINVAL, "theta, Y, dY and dtheta must be non-NULL");
+    if (!theta || !dtheta || (m > 0 && (!Y || !dY))) return fail(GIVENS_EINVAL, "theta, Y, dY and dtheta must be non-NULL");
     if (ldy < m || lddy < m || (dX && lddx < m)) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (dX && dX == dY && lddx != lddy) return fail(GIVENS_EINVAL, "in-place dX needs lddx == lddy");
     Cfg c = make_cfg(n);
