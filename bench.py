@@ -478,7 +478,7 @@ def main():
                                        "(max boost; DESIGN.md §5)",
                          "flops_per_rotation_column": FLOPS_BWD, "ms_per_launch": ms_bwd},
             "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd,
-            "gpu_launches": 7 * args.steps,
+            "gpu_launches": 8 * args.steps,
             "clocks": clk,
         }
         if e2e:

@@ -3,7 +3,7 @@
 // (or I to build U), and the replay backward with a deterministic dtheta reduction.
 //
 // Kernels (DESIGN.md §4 lists the roofline and algorithmic bytes of each):
-//   k_flip / k_sigma / k_coef  per-call coefficient precompute (fp64 trig, pi-reduction, sign
+//   k_flip / k_sigma_* / k_coef  per-call coefficient precompute (fp64 trig, pi-reduction, sign
 //                              bookkeeping) into the ring kernels' lane-chunked table layout;
 //   k_ring<W,L,MODE>           the hot path: one CTA owns a column slab, every block b_r runs
 //                              on-chip from registers, coefficients stream in by TMA bulk copies;
@@ -172,7 +172,7 @@ int64_t grid_for(const Cfg &c, int mode0, int64_t m) {
 }
 
 struct WsLayout {
-    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, lay, partial, scratch, total;
+    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, segx, lay, partial, scratch, total;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
@@ -194,6 +194,7 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     L.flip = off; off = al256(off + (size_t)c.R * c.S);
     L.sig = off; off = al256(off + (size_t)c.R * c.ne);
     L.sfin = off; off = al256(off + (size_t)c.ne);
+    L.segx = off; off = al256(off + (size_t)32 * c.ne);
     L.lay = off; off = al256(off + (size_t)(c.ne + 2) * 4);
     L.partial = off;
     if (base == GIVENS_OP_BACKWARD) {
@@ -251,40 +252,41 @@ __global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uin
 
 // (2) per row: parity of flips among the blocks applied before block r in forward order
 // (forward applies b_R first), i.e. blocks r' > r. sig[r][row], sfin[row].
-// One warp per row: lane l owns a contiguous segment of blocks (highest blocks in lane 0); an
-// exclusive prefix XOR over the lanes gives each segment its starting parity.
+// The R blocks are cut into 32 contiguous segments (segment 0 = the highest blocks); thread
+// (row i, segment c) walks its segment: k_sigma_seg stores the segment's XOR, k_sigma_fill
+// starts from the XOR of the segments before it and writes sig. Consecutive threads take
+// consecutive rows, whose slots in a block are adjacent, so the flip reads are coalesced.
 // A reflection D (applied before every block) flips the parity of its label in every block and
 // in sfin; the kernels then load and store without knowing about it.
-__global__ void k_sigma(int ne, const uint8_t *__restrict__ flip, const int32_t *__restrict__ lay,
-                        uint8_t *__restrict__ sig, uint8_t *__restrict__ sfin) {
-    const int S = ne / 2, R = ne - 1;
-    const int lane = threadIdx.x & 31;
-    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+__device__ __forceinline__ uint32_t flip_of(const uint8_t *__restrict__ flip, int i, int r, int ne) {
+    const int p = pos_of(i, r, ne);
+    const int k = p < ne - 1 - p ? p : ne - 1 - p;
+    return (uint32_t)flip[(int64_t)r * (ne / 2) + k];
+}
+
+__global__ void k_sigma_seg(int ne, const uint8_t *__restrict__ flip, uint8_t *__restrict__ segx) {
+    const int R = ne - 1, i = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
     if (i >= ne) return;
-    const int seg = (R + 31) / 32;
-    const int hi = R - 1 - lane * seg;          // first (highest) block of this lane's segment
-    const int lo = max(hi - seg + 1, 0);
-    auto flip_at = [&](int r) {
-        int p = pos_of(i, r, ne);
-        int k = p < ne - 1 - p ? p : ne - 1 - p;
-        return (uint32_t)flip[(int64_t)r * S + k];
-    };
+    const int seg = (R + 31) / 32, hi = R - 1 - c * seg, lo = max(hi - seg + 1, 0);
     uint32_t x = 0;
-    for (int r = hi; r >= lo; r--) x ^= flip_at(r);
-    // exclusive prefix XOR over lanes 0..lane-1
-    uint32_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl ^= v;
-    }
+    for (int r = hi; r >= lo; r--) x ^= flip_of(flip, i, r, ne);
+    segx[(int64_t)c * ne + i] = (uint8_t)x;
+}
+
+__global__ void k_sigma_fill(int ne, const uint8_t *__restrict__ flip, const uint8_t *__restrict__ segx,
+                             const int32_t *__restrict__ lay, uint8_t *__restrict__ sig, uint8_t *__restrict__ sfin) {
+    const int R = ne - 1, i = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+    if (i >= ne) return;
+    const int seg = (R + 31) / 32, hi = R - 1 - c * seg, lo = max(hi - seg + 1, 0);
+    uint32_t par = 0;
+    for (int cc = 0; cc < c; cc++) par ^= segx[(int64_t)cc * ne + i];
     const uint32_t rf = (lay[ne + 1] == i) ? 1u : 0u;
-    uint32_t par = incl ^ x ^ rf;
+    if (c == 31) sfin[i] = (uint8_t)(par ^ segx[(int64_t)31 * ne + i] ^ rf);
+    par ^= rf;
     for (int r = hi; r >= lo; r--) {
         sig[(int64_t)r * ne + i] = (uint8_t)par;
-        par ^= flip_at(r);
+        par ^= flip_of(flip, i, r, ne);
     }
-    if (lane == 31) sfin[i] = (uint8_t)(incl ^ rf);
 }
 
 __device__ __forceinline__ int coef_pos(int k, int W, int L) {
@@ -747,8 +749,13 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
     CUDA_TRY(cudaGetLastError());
     k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, lay, ws + L.flip);
     CUDA_TRY(cudaGetLastError());
-    k_sigma<<<(unsigned)((c.ne + 7) / 8), 256, 0, st>>>(c.ne, ws + L.flip, lay, ws + L.sig, ws + L.sfin);
-    CUDA_TRY(cudaGetLastError());
+    {
+        const dim3 grid((unsigned)((c.ne + 127) / 128), 32);
+        k_sigma_seg<<<grid, 128, 0, st>>>(c.ne, ws + L.flip, ws + L.segx);
+        CUDA_TRY(cudaGetLastError());
+        k_sigma_fill<<<grid, 128, 0, st>>>(c.ne, ws + L.flip, ws + L.segx, lay, ws + L.sig, ws + L.sfin);
+        CUDA_TRY(cudaGetLastError());
+    }
     int64_t tot = (int64_t)(c.R + 2) * c.S;
     int W = c.fast ? c.W : c.S, Lq = c.fast ? c.La : 1;
     k_coef<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, c.rowbytes, theta, mask, ws + L.flip,

@@ -17,9 +17,9 @@ with open(os.path.join(pr, f"{tag}_launches.csv"), "w") as f:
     f.write("id,kernel,gpu__time_duration_ns\n")
     for i, k, v in rows:
         f.write(f"{i},{k},{v:.0f}\n")
-# last full step (launches after warm-up): 7 launches per step (k_layout, k_flip, k_sigma, k_coef, fwd, bwd, reduce)
+# last full step (launches after warm-up): 8 launches per step (k_layout, k_flip, k_sigma_seg, k_sigma_fill, k_coef, fwd, bwd, reduce)
 tot = collections.Counter()
-for i, k, v in rows[-7:]:
+for i, k, v in rows[-8:]:
     tot[k] += v
 T = sum(tot.values())
 share = {k: {"ns": v, "share": v / T} for k, v in tot.items()}
