@@ -151,6 +151,40 @@ struct RingArgs {
 
 template <int K>
 struct ColIO;
+// whole-slab fast path (every column in range, K-aligned rows): unconditional vector accesses, so
+// a slab load is one batch of independent LDGs instead of a chain of branch regions that each wait
+// for their load
+template <int K>
+struct FastIO {
+    using IO = ColIO<K>;
+    using V = typename IO::V;
+    static constexpr int KP = IO::KP;
+    __device__ static void load(const float *p, V (&v)[KP]) {
+        if constexpr (K == 1) {
+            v[0] = __ldg(p);
+        } else if constexpr (K == 2) {
+            v[0] = __ldg(reinterpret_cast<const float2 *>(p));
+        } else {
+#pragma unroll
+            for (int h = 0; h < K / 4; h++) {
+                const float4 a = __ldg(reinterpret_cast<const float4 *>(p) + h);
+                v[2 * h] = make_float2(a.x, a.y);
+                v[2 * h + 1] = make_float2(a.z, a.w);
+            }
+        }
+    }
+    __device__ static void store(float *p, const V (&v)[KP]) {
+        if constexpr (K == 1) {
+            *p = v[0];
+        } else if constexpr (K == 2) {
+            *reinterpret_cast<float2 *>(p) = v[0];
+        } else {
+#pragma unroll
+            for (int h = 0; h < K / 4; h++)
+                reinterpret_cast<float4 *>(p)[h] = make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
+        }
+    }
+};
 template <>
 struct ColIO<1> {
     using V = float;
@@ -500,6 +534,22 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         __syncwarp();
     };
 
+    // final signs (sigma) of the labels this lane holds in the s_{R-1} layout -- the
+    // forward's store layout and the backward's / transpose's load layout: bit q top, bit W+q bottom
+    uint64_t smask = 0;
+#pragma unroll
+    for (int q = 0; q < W; q++) {
+        const int k = t * W + q;
+        const int lt = row_sRm1(k, ne), lb = row_sRm1(ne - 1 - k, ne);
+        if (active) {
+            const int rt = a.lrow ? a.lrow[lt] : lt, rb = a.lrow ? a.lrow[lb] : lb;
+            if (rt < n && a.sfin[lt]) smask |= 1ull << q;
+            if (rb < n && a.sfin[lb]) smask |= 1ull << (W + q);
+        }
+    }
+    auto sneg_t = [&](int q) { return ((smask >> q) & 1ull) != 0; };
+    auto sneg_b = [&](int q) { return ((smask >> (W + q)) & 1ull) != 0; };
+
     int gst = 0;    // coefficient stages consumed by this CTA
     int grp = 0;    // dtheta ring groups completed by this CTA
     V ZT[KP][W], ZB[KP][W];
@@ -507,7 +557,37 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
 
     for (int64_t slab = blockIdx.x; slab < a.nslabs; slab += gridDim.x) {
         const int64_t col0 = slab * C + (int64_t)(cw * LC + g) * K;
+        // uniform over the CTA: every column of the slab in range, vector-aligned rows, identity layout
+        const bool fast = a.vec_ok && a.lrow == nullptr && (slab + 1) * C <= a.m;
         // ---------------- load the slab into the start layout (s_0 forward, s_{R-1} backward)
+        if (BM != M_BUILDU && fast) {
+            // rows >= n (the odd-n bye, idle lanes) read row 0 and are zeroed after the load
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+                const int k = t * W + q;
+                int rt = UP ? row_sRm1(k, ne) : row_s0(k), rb = UP ? row_sRm1(ne - 1 - k, ne) : row_s0(ne - 1 - k);
+                if (!active) rt = rb = n;
+                const bool zt = rt >= n, zb = rb >= n;
+                V vt[KP], vb[KP];
+                FastIO<K>::load(a.X + (int64_t)(zt ? 0 : rt) * a.ldx + col0, vt);
+                FastIO<K>::load(a.X + (int64_t)(zb ? 0 : rb) * a.ldx + col0, vb);
+                const bool nt = UP && sneg_t(q), nb = UP && sneg_b(q);
+#pragma unroll
+                for (int p = 0; p < KP; p++) {
+                    ZT[p][q] = zt ? V{} : vneg_if(vt[p], nt);
+                    ZB[p][q] = zb ? V{} : vneg_if(vb[p], nb);
+                }
+                if constexpr (GRAD) {
+                    FastIO<K>::load(a.dY + (int64_t)(zt ? 0 : rt) * a.lddy + col0, vt);
+                    FastIO<K>::load(a.dY + (int64_t)(zb ? 0 : rb) * a.lddy + col0, vb);
+#pragma unroll
+                    for (int p = 0; p < KP; p++) {
+                        DT[p][q] = zt ? V{} : vneg_if(vt[p], nt);
+                        DB[p][q] = zb ? V{} : vneg_if(vb[p], nb);
+                    }
+                }
+            }
+        } else
 #pragma unroll
         for (int q = 0; q < W; q++) {
             const int k = t * W + q;
@@ -539,7 +619,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
             }
             if (UP) {
-                const bool nt = rt < n && a.sfin[lt], nb = rb < n && a.sfin[lb];
+                const bool nt = sneg_t(q), nb = sneg_b(q);
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }
@@ -550,7 +630,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else for (int p = 0; p < KP; p++) vt[p] = V{};
                 if (rb < n) IO::load(a.dY + (int64_t)rb * a.lddy, col0, a.m, a.vec_ok, vb);
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
-                const bool nt = rt < n && a.sfin[lt], nb = rb < n && a.sfin[lb];
+                const bool nt = sneg_t(q), nb = sneg_b(q);
 #pragma unroll
                 for (int p = 0; p < KP; p++) {
                     DT[p][q] = vneg_if(vt[p], nt);
@@ -783,6 +863,23 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
 
         // ---------------- store from the end layout (s_{R-1} forward, s_0 backward)
         if (BM == M_BWD && a.Y == nullptr) continue;
+        if (fast) {
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+                const int k = t * W + q;
+                const int rt = UP ? row_s0(k) : row_sRm1(k, ne), rb = UP ? row_s0(ne - 1 - k) : row_sRm1(ne - 1 - k, ne);
+                V vt[KP], vb[KP];
+                const bool nt = !UP && sneg_t(q), nb = !UP && sneg_b(q);
+#pragma unroll
+                for (int p = 0; p < KP; p++) {
+                    if constexpr (GRAD) { vt[p] = DT[p][q]; vb[p] = DB[p][q]; }
+                    else { vt[p] = vneg_if(ZT[p][q], nt); vb[p] = vneg_if(ZB[p][q], nb); }
+                }
+                if (active && rt < n) FastIO<K>::store(a.Y + (int64_t)rt * a.ldy + col0, vt);
+                if (active && rb < n) FastIO<K>::store(a.Y + (int64_t)rb * a.ldy + col0, vb);
+            }
+            continue;
+        }
 #pragma unroll
         for (int q = 0; q < W; q++) {
             const int k = t * W + q;
@@ -799,7 +896,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else { vt[p] = ZT[p][q]; vb[p] = ZB[p][q]; }
             }
             if (!UP) {
-                const bool nt = rt < n && a.sfin[lt], nb = rb < n && a.sfin[lb];
+                const bool nt = sneg_t(q), nb = sneg_b(q);
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }
