@@ -505,12 +505,30 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             }
             ob[r * OUTCH + c] = make_float4(lo.x, lo.y, hi.x, hi.y);
         };
+        // pairwise tree over the NSUM warps (fixed order, depth log2 NSUM), all loads of an item
+        // issued before the first add
+        auto tree_item = [&](int r, int c) {
+            const float4 *src = rsrc + (size_t)r * NCHW + c;
+            float4 v[NSUM];
+#pragma unroll
+            for (int w = 0; w < NSUM; w++) v[w] = src[(size_t)w * H * D * NCHW];
+#pragma unroll
+            for (int st = 1; st < NSUM; st <<= 1) {
+#pragma unroll
+                for (int w = 0; w + st < NSUM; w += 2 * st) {
+                    const float2 lo = __fadd2_rn(make_float2(v[w].x, v[w].y), make_float2(v[w + st].x, v[w + st].y));
+                    const float2 hi = __fadd2_rn(make_float2(v[w].z, v[w].w), make_float2(v[w + st].z, v[w + st].w));
+                    v[w] = make_float4(lo.x, lo.y, hi.x, hi.y);
+                }
+            }
+            ob[r * OUTCH + c] = v[0];
+        };
         if constexpr (EVEN) {
             constexpr int ITEMS = RG * OUTCH;
 #pragma unroll
             for (int j = 0; j < (ITEMS + 31) / 32; j++) {
                 const int it = lane + 32 * j;
-                if (ITEMS % 32 == 0 || it < ITEMS) sum_item(it / OUTCH, it % OUTCH);
+                if (ITEMS % 32 == 0 || it < ITEMS) tree_item(it / OUTCH, it % OUTCH);
             }
         } else {
             for (int it = lane; it < RG * nch; it += 32) sum_item(it / nch, it % nch);
