@@ -528,7 +528,10 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
 #pragma unroll
             for (int j = 0; j < (ITEMS + 31) / 32; j++) {
                 const int it = lane + 32 * j;
-                if (ITEMS % 32 == 0 || it < ITEMS) tree_item(it / OUTCH, it % OUTCH);
+                if (ITEMS % 32 == 0 || it < ITEMS) {
+                    if constexpr (UNI) sum_item(it / OUTCH, it % OUTCH);  // (registers: the tree spills there)
+                    else tree_item(it / OUTCH, it % OUTCH);
+                }
             }
         } else {
             for (int it = lane; it < RG * nch; it += 32) sum_item(it / nch, it % nch);
@@ -554,9 +557,11 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
 
     // final signs (sigma) of the labels this lane holds in the s_{R-1} layout -- the
     // forward's store layout and the backward's / transpose's load layout: bit q top, bit W+q bottom
+    // (the unitary variant keeps per-slab sfin loads and the general slab path: its register
+    // budget is tighter, and the mask measured slower there)
     uint64_t smask = 0;
 #pragma unroll
-    for (int q = 0; q < W; q++) {
+    for (int q = 0; q < (UNI ? 0 : W); q++) {
         const int k = t * W + q;
         const int lt = row_sRm1(k, ne), lb = row_sRm1(ne - 1 - k, ne);
         if (active) {
@@ -567,6 +572,12 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     }
     auto sneg_t = [&](int q) { return ((smask >> q) & 1ull) != 0; };
     auto sneg_b = [&](int q) { return ((smask >> (W + q)) & 1ull) != 0; };
+    auto sgn_t = [&](int q, int lt, int rt) -> bool {
+        if constexpr (UNI) return rt < n && a.sfin[lt]; else return sneg_t(q);
+    };
+    auto sgn_b = [&](int q, int lb, int rb) -> bool {
+        if constexpr (UNI) return rb < n && a.sfin[lb]; else return sneg_b(q);
+    };
 
     int gst = 0;    // coefficient stages consumed by this CTA
     int grp = 0;    // dtheta ring groups completed by this CTA
@@ -576,7 +587,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     for (int64_t slab = blockIdx.x; slab < a.nslabs; slab += gridDim.x) {
         const int64_t col0 = slab * C + (int64_t)(cw * LC + g) * K;
         // uniform over the CTA: every column of the slab in range, vector-aligned rows, identity layout
-        const bool fast = a.vec_ok && a.lrow == nullptr && (slab + 1) * C <= a.m;
+        const bool fast = !UNI && a.vec_ok && a.lrow == nullptr && (slab + 1) * C <= a.m;
         // ---------------- load the slab into the start layout (s_0 forward, s_{R-1} backward)
         if (BM != M_BUILDU && fast) {
             // rows >= n (the odd-n bye, idle lanes) read row 0 and are zeroed after the load
@@ -637,7 +648,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
             }
             if (UP) {
-                const bool nt = sneg_t(q), nb = sneg_b(q);
+                const bool nt = sgn_t(q, lt, rt), nb = sgn_b(q, lb, rb);
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }
@@ -648,7 +659,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else for (int p = 0; p < KP; p++) vt[p] = V{};
                 if (rb < n) IO::load(a.dY + (int64_t)rb * a.lddy, col0, a.m, a.vec_ok, vb);
                 else for (int p = 0; p < KP; p++) vb[p] = V{};
-                const bool nt = sneg_t(q), nb = sneg_b(q);
+                const bool nt = sgn_t(q, lt, rt), nb = sgn_b(q, lb, rb);
 #pragma unroll
                 for (int p = 0; p < KP; p++) {
                     DT[p][q] = vneg_if(vt[p], nt);
@@ -914,7 +925,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 else { vt[p] = ZT[p][q]; vb[p] = ZB[p][q]; }
             }
             if (!UP) {
-                const bool nt = sneg_t(q), nb = sneg_b(q);
+                const bool nt = sgn_t(q, lt, rt), nb = sgn_b(q, lb, rb);
 #pragma unroll
                 for (int p = 0; p < KP; p++) { vt[p] = vneg_if(vt[p], nt); vb[p] = vneg_if(vb[p], nb); }
             }
