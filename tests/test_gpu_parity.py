@@ -181,6 +181,33 @@ def test_strided_leading_dimension(g):
     assert rel(Y, oracle.apply(n, th, X.astype(np.float64))) <= TOL_Y
 
 
+@pytest.mark.parametrize("n", [8, 64, 255, 256, 1024, 2047, 4096])
+def test_fast_slab_path_bitwise(g, n):
+    """The whole-slab fast load/store path (aligned rows, every column in range) and the general
+    path (rows misaligned by one float, per-element checks) run the same arithmetic in the same
+    slab decomposition: Y, dX and dtheta must agree bit for bit."""
+    m = 4096
+    th, X, dY, _ = _inputs(n, m, seed=21)
+    tt, Xc, dYc = _cuda(th), _cuda(X), _cuda(dY)
+    Y0 = g.apply(tt, Xc)
+    dth0, dX0 = g.backward(tt, Y0, dYc)
+
+    def shifted(a):  # same values, base pointer 4 bytes past a 16-byte boundary
+        buf = torch.zeros(a.shape[0] * (m + 4) + 4, device="cuda")
+        v = buf[1:1 + a.shape[0] * (m + 4)].view(a.shape[0], m + 4)[:, :m]
+        v.copy_(a)
+        return v
+    Xs, dYs = shifted(Xc), shifted(dYc)
+    Ys = shifted(torch.zeros_like(Xc))
+    g.apply(tt, Xs, out=Ys)
+    dXs = shifted(torch.zeros_like(Xc))
+    dths, _ = g.backward(tt, Ys, dYs, dX=dXs)
+    torch.cuda.synchronize()
+    assert torch.equal(Ys, Y0)
+    assert torch.equal(dXs, dX0)
+    assert torch.equal(dths, dth0)
+
+
 # ---------------------------------------------------------------- full-size configurations
 
 def _closed_form_block_dtheta(g, n, Y, dY, r_block):

@@ -1,4 +1,4 @@
-// Microbenchmark: FFMA2 throughput vs operand pattern (register scalar, immediate, pair coefficient, scalar FFMA, shared scalar). DESIGN.md §10.
+// Microbenchmark: FFMA2 throughput vs operand pattern (immediate, register scalar, pair coefficient, scalar FFMA, shared scalar, FSEL-interleaved). DESIGN.md §10a.
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -36,6 +36,13 @@ __global__ void __launch_bounds__(256, 1) k(float *out, const float *__restrict_
                 y[i].y = fmaf(c[(i + 1) % NCH], x[i].y, y[i].y);
                 x[i].x = fmaf(c[i], y[i].x, x[i].x);
                 x[i].y = fmaf(c[i], y[i].y, x[i].y);
+            } else if (MODE == 5) {  // immediates + 2 FSEL per FFMA2 on the same data
+                x[i] = __ffma2_rn(make_float2(0.01f * i, 0.01f * i), y[i], x[i]);
+                const bool pr = c[i] > 0.f;
+                float2 t = make_float2(pr ? x[i].x : y[i].x, pr ? x[i].y : y[i].y);
+                y[i] = __ffma2_rn(make_float2(-0.02f * i, -0.02f * i), t, y[i]);
+                t = make_float2(pr ? y[i].x : x[i].x, pr ? y[i].y : x[i].y);
+                x[i] = __ffma2_rn(make_float2(0.01f * i, 0.01f * i), t, x[i]);
             } else if (MODE == 4) {  // FMUL2-free: scalar register coefficient shared by 2 packs (reuse)
                 const int j = (i + NCH / 2) % NCH;
                 x[i] = __ffma2_rn(make_float2(c[i], c[i]), y[i], x[i]);
@@ -74,6 +81,6 @@ int main() {
     float *out, *cin; cudaMalloc(&out, 4); cudaMalloc(&cin, 256);
     float h[64]; for (int i = 0; i < 64; i++) h[i] = 0.01f * (i + 1);
     cudaMemcpy(cin, h, 256, cudaMemcpyHostToDevice);
-    run<0>(out, cin); run<1>(out, cin); run<2>(out, cin); run<3>(out, cin); run<4>(out, cin);
+    run<0>(out, cin); run<1>(out, cin); run<2>(out, cin); run<3>(out, cin); run<4>(out, cin); run<5>(out, cin);
     return 0;
 }
