@@ -239,6 +239,45 @@ def small_config_line(g, torch, synth, dev, n=256, m=4096, reps=20):
             "bwd_ms": round(tb, 4), "rotations_per_s": N * m / ((tf + tb) * 1e-3)}
 
 
+def c5_shard_line(g, torch, synth, dev, n=2047, m=32768, m_keep=1024, reps=5):
+    """BASELINE config C5 as one rank of its 8-GPU run: n = 2047 (odd: the bye vertex), the rank's
+    m = 262144 / 8 = 32768 columns, the SURVEY §5 restriction mask m_keep = 1024 (pinned angles are
+    identity rotations, dtheta = 0). Device ms of apply + backward (dX, dtheta), mean of `reps`
+    after warm-up, L2 flushed before each. Rates count active (unpinned) angles."""
+    N = n * (n - 1) // 2
+    th = torch.from_numpy(synth.theta(N, seed=SEED)).to(dev)
+    mask = torch.from_numpy(g.mask_from_keep(n, m_keep)).to(dev)
+    X = torch.from_numpy(synth.normal_matrix(n, m, SEED, synth.TID_X)).to(dev)
+    dY = torch.from_numpy(synth.normal_matrix(n, m, SEED, synth.TID_DY)).to(dev)
+    ws = g.workspace(g.OP_BACKWARD, n, m, dev)
+    Y, dX, dth = torch.empty_like(X), torch.empty_like(X), torch.empty(N, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(2):
+        g.apply(th, X, mask=mask, out=Y, ws=ws)
+        g.backward(th, Y, dY, mask=mask, ws=ws, recompute=False, dtheta=dth, dX=dX)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    tf = tb = 0.0
+    for _ in range(reps):
+        flush.fill_(1.0)
+        ev[0].record()
+        g.apply(th, X, mask=mask, out=Y, ws=ws)
+        ev[1].record()
+        g.backward(th, Y, dY, mask=mask, ws=ws, recompute=False, dtheta=dth, dX=dX)
+        ev[2].record()
+        torch.cuda.synchronize()
+        tf += ev[0].elapsed_time(ev[1])
+        tb += ev[1].elapsed_time(ev[2])
+    tf, tb = tf / reps, tb / reps
+    active = int(mask.sum().item())  # 1 = free angle (include/givens.h)
+    ne = n + (n & 1)
+    executed = (ne - 1) * (ne // 2)  # every slot of every block runs, pinned and bye ones as identities
+    return {"workload": f"C5 one rank of 8: n={n} (odd), m={m} of 262144 columns, mask m_keep={m_keep}: "
+                        "apply + backward (dX, dtheta)",
+            "fwd_ms": round(tf, 4), "bwd_ms": round(tb, 4), "active_angles": active, "executed_slots": executed,
+            "active_rotations_per_s": active * m / ((tf + tb) * 1e-3),
+            "executed_rotations_per_s": executed * m / ((tf + tb) * 1e-3)}
+
+
 def unitary_line(g, torch, synth, dev, peak_tflops, n=1024, m=32768, reps=5):
     """the unitary U(n) path (Appendix A) at n = 1024 on m complex columns (the same
     2m = 65536 real columns as C3): device ms of u_apply and u_backward, mean of `reps` after
@@ -487,6 +526,7 @@ def main():
             out["ubuild_ms_vs_n"] = ubuild
         if world == 1 and not args.no_ubuild:
             out["c2"] = small_config_line(g, torch, synth, dev)
+            out["c5_shard"] = c5_shard_line(g, torch, synth, dev)
             out["unitary"] = unitary_line(g, torch, synth, dev, peak)
             bf16 = _measured_peak("bf16_tflops", 2250.0)
             out["f2_gemm_path"] = gemm_path_line(g, torch, theta, X, dY, n, m, ms_step, bf16 / 2)
