@@ -330,17 +330,20 @@ struct RingGeom {
     // (forward / adjoint apply: the phases as two FFMA2-ready pairs per side, 32 B)
     static constexpr int PHB = UNI ? (GRAD ? 16 : 32) : 0;  // phase bytes per slot
     static constexpr int RB = 8 + PHB + ((UNI && GRAD) ? 8 : 0);
-    // table rows per TMA stage: a power of two dividing W/2, stages of <= 32 KB forward and
-    // <= 16 KB next to the dtheta ring
+    // table rows per TMA stage: a power of two dividing W (real apply: up to one stage per unrolled
+    // body of W steps, stages of <= 64 KB -- each stage boundary costs a wait and a release; 4.61 ->
+    // 4.41 ms at C3 against 8-row stages) or W/2 (stages of <= 16 KB next to the backward's dtheta
+    // ring, <= 40 KB for the unitary apply)
     static constexpr int sps_pick() {
-        int v = W / 2;
-        while (v > 1 && v * S * RB > (GRAD ? 16384 : (UNI ? 40960 : 32768))) v /= 2;
+        int v = (GRAD || UNI) ? W / 2 : W;
+        while (v > 1 && v * S * RB > (GRAD ? 16384 : (UNI ? 40960 : 65536))) v /= 2;
         return v;
     }
     static constexpr int SPS = sps_pick();
     static constexpr int STAGEB = SPS * S * RB;
-    // stages in flight: 64 KB of table buffers next to the backward's dtheta ring, 96 KB otherwise
-    static constexpr int NSTAGE_ = (GRAD ? 65536 : (UNI ? 163840 : 98304)) / STAGEB;
+    // stages in flight: 64 KB of table buffers next to the backward's dtheta ring, 160 KB for the
+    // unitary apply, 192 KB for the real apply
+    static constexpr int NSTAGE_ = (GRAD ? 65536 : (UNI ? 163840 : 196608)) / STAGEB;
     static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
     // backward sums (dtheta, and dphi in the unitary variant): per-warp ring of NG groups of RG
     // steps, reduced one group later
