@@ -332,11 +332,13 @@ struct RingGeom {
     static constexpr int RB = 8 + PHB + ((UNI && GRAD) ? 8 : 0);
     // table rows per TMA stage: a power of two dividing W (real apply: up to one stage per unrolled
     // body of W steps, stages of <= 64 KB -- each stage boundary costs a wait and a release; 4.61 ->
-    // 4.41 ms at C3 against 8-row stages) or W/2 (stages of <= 16 KB next to the backward's dtheta
-    // ring, <= 40 KB for the unitary apply)
+    // 4.41 ms at C3 against 8-row stages) or W/2 next to the backward's dtheta ring (64 KB of stages:
+    // two of <= 32 KB for the real backward -- C3 bwd 7.95 -> 7.86 ms and n = 2048 42.6 -> 40.7 ms on
+    // 32768 columns against four of 16 KB -- four of <= 16 KB for the unitary one), <= 40 KB for the
+    // unitary apply
     static constexpr int sps_pick() {
         int v = (GRAD || UNI) ? W / 2 : W;
-        while (v > 1 && v * S * RB > (GRAD ? 16384 : (UNI ? 40960 : 65536))) v /= 2;
+        while (v > 1 && v * S * RB > (GRAD ? (UNI ? 16384 : 32768) : (UNI ? 40960 : 65536))) v /= 2;
         return v;
     }
     static constexpr int SPS = sps_pick();
