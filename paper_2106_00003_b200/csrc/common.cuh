@@ -330,23 +330,6 @@ struct RingGeom {
     // (forward / adjoint apply: the phases as two FFMA2-ready pairs per side, 32 B)
     static constexpr int PHB = UNI ? (GRAD ? 16 : 32) : 0;  // phase bytes per slot
     static constexpr int RB = 8 + PHB + ((UNI && GRAD) ? 8 : 0);
-    // table rows per TMA stage: a power of two dividing W (real apply: up to one stage per unrolled
-    // body of W steps, stages of <= 64 KB -- each stage boundary costs a wait and a release; 4.61 ->
-    // 4.41 ms at C3 against 8-row stages) or W/2 next to the backward's dtheta ring (64 KB of stages:
-    // two of <= 32 KB for the real backward -- C3 bwd 7.95 -> 7.86 ms and n = 2048 42.6 -> 40.7 ms on
-    // 32768 columns against four of 16 KB -- four of <= 16 KB for the unitary one), <= 40 KB for the
-    // unitary apply
-    static constexpr int sps_pick() {
-        int v = (GRAD || UNI) ? W / 2 : W;
-        while (v > 1 && v * S * RB > (GRAD ? (UNI ? 16384 : 32768) : (UNI ? 40960 : 65536))) v /= 2;
-        return v;
-    }
-    static constexpr int SPS = sps_pick();
-    static constexpr int STAGEB = SPS * S * RB;
-    // stages in flight: 64 KB of table buffers next to the backward's dtheta ring, 160 KB for the
-    // unitary apply, 192 KB for the real apply
-    static constexpr int NSTAGE_ = (GRAD ? 65536 : (UNI ? 163840 : 196608)) / STAGEB;
-    static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
     // backward sums (dtheta, and dphi in the unitary variant): per-warp ring of NG groups of RG
     // steps, reduced one group later
     static constexpr int VALS = UNI ? 2 : 1;
@@ -358,9 +341,33 @@ struct RingGeom {
     static constexpr int NSUM = NW / H;             // warps contributing to each chunk
     static constexpr int OUTCH = (NCHW + NSUM - 1) / NSUM;  // chunks reduced per warp (max)
     static constexpr int XV = GRAD ? 2 * KP : KP;   // packed values crossing a warp boundary per direction
+    static constexpr size_t XB = H > 1 ? (size_t)2 * NW * 2 * XV * 8 : 0;  // warp-boundary exchange
+    static constexpr size_t REDB = GRAD ? (size_t)NW * D * NCHW * 16 + (size_t)NW * NG * RG * OUTCH * 16 : 0;
+    // Coefficient stages. Each stage boundary costs a wait and a release, so stages are as large as
+    // shared memory allows: the real apply stages up to one unrolled body of W table rows (<= 64 KB
+    // each, 192 KB in flight; 4.61 -> 4.41 ms at C3 against 8-row stages); the real backward takes
+    // what its dtheta ring leaves (<= 128 KB, two or more stages; C3: two of 32 KB instead of four of 16 KB,
+    // 7.95 -> 7.86 ms, n = 2048: 42.6 -> 40.7 ms on 32768 columns); the unitary variant keeps W/2-row
+    // stages of <= 40 KB for the apply (the backward's tables are 32 B per slot: 16 KB per step at
+    // S = 512, so 16 KB stages meant a boundary every step).
+    static constexpr int GRAD_BUDGET_() {
+        const long free_ = 225 * 1024 - 256 - (long)XB - (long)REDB;
+        return (int)(free_ < 131072 ? free_ : 131072);
+    }
+    static constexpr int STAGE_BUDGET = GRAD ? GRAD_BUDGET_() : (UNI ? 163840 : 196608);
+    static constexpr int sps_pick() {
+        int v = (GRAD || UNI) ? W / 2 : W;
+        const int lim = GRAD ? STAGE_BUDGET / 2 : (UNI ? 40960 : 65536);
+        while (v > 1 && v * S * RB > lim) v /= 2;
+        return v;
+    }
+    static constexpr int SPS = sps_pick();
+    static constexpr int STAGEB = SPS * S * RB;
+    static constexpr int NSTAGE_ = STAGE_BUDGET / STAGEB;
+    static constexpr int NSTAGE = NSTAGE_ > 8 ? 8 : (NSTAGE_ < 2 ? 2 : NSTAGE_);
     static constexpr size_t OFF_STAGE = 256;
     static constexpr size_t OFF_X = OFF_STAGE + (size_t)NSTAGE * STAGEB;
-    static constexpr size_t OFF_RED = OFF_X + (H > 1 ? (size_t)2 * NW * 2 * XV * 8 : 0);
+    static constexpr size_t OFF_RED = OFF_X + XB;
     static constexpr size_t OFF_OUT = OFF_RED + (GRAD ? (size_t)NW * D * NCHW * 16 : 0);
     static constexpr size_t SMEM = OFF_OUT + (GRAD ? (size_t)NW * NG * RG * OUTCH * 16 : 0);
 };
