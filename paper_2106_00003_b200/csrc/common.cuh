@@ -800,12 +800,17 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                             }
                         }
                     }
+                    // warps w and w+4 share an SMSP: the low half reduces the previous group at step
+                    // LO of this one, the high half at RG/2 - 1, so one of them keeps the FMA pipe busy;
+                    // LO = RG - 2 (not the group's last step) leaves the low half a step of slack
+                    // before the next group's rempty wait (C3 bwd 15.74 -> 15.63 ms)
+                    constexpr int LO = RG >= 4 ? RG - 2 : RG - 1;
+                    if constexpr (r == LO) {
+                        if (((warp >> 2) & 1) == 0 && grp >= 1) reduce_group(grp - 1);
+                    }
                     if constexpr (r == RG - 1) {
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&rfull[bi]);
-                        // warps w and w+4 share an SMSP: the low half reduces the previous group
-                        // here, the high half RG/2 steps earlier, so one of them keeps the FMA pipe busy
-                        if (((warp >> 2) & 1) == 0 && grp >= 1) reduce_group(grp - 1);
                         grp++;
                     }
                     if constexpr (r == RG / 2 - 1) {
