@@ -535,7 +535,36 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             }
             ob[r * OUTCH + c] = v[0];
         };
-        if constexpr (EVEN) {
+        // two items per pass when the items split into pairs: 2 NSUM loads in flight before the first
+        // add (C3 bwd 15.65 -> 15.53 ms)
+        auto tree_pair = [&](int i0, int i1) {
+            const float4 *s0 = rsrc + (size_t)(i0 / OUTCH) * NCHW + (i0 % OUTCH);
+            const float4 *s1 = rsrc + (size_t)(i1 / OUTCH) * NCHW + (i1 % OUTCH);
+            float4 v[NSUM], u[NSUM];
+#pragma unroll
+            for (int w = 0; w < NSUM; w++) {
+                v[w] = s0[(size_t)w * H * D * NCHW];
+                u[w] = s1[(size_t)w * H * D * NCHW];
+            }
+#pragma unroll
+            for (int st = 1; st < NSUM; st <<= 1) {
+#pragma unroll
+                for (int w = 0; w + st < NSUM; w += 2 * st) {
+                    float2 lo = __fadd2_rn(make_float2(v[w].x, v[w].y), make_float2(v[w + st].x, v[w + st].y));
+                    float2 hi = __fadd2_rn(make_float2(v[w].z, v[w].w), make_float2(v[w + st].z, v[w + st].w));
+                    v[w] = make_float4(lo.x, lo.y, hi.x, hi.y);
+                    lo = __fadd2_rn(make_float2(u[w].x, u[w].y), make_float2(u[w + st].x, u[w + st].y));
+                    hi = __fadd2_rn(make_float2(u[w].z, u[w].w), make_float2(u[w + st].z, u[w + st].w));
+                    u[w] = make_float4(lo.x, lo.y, hi.x, hi.y);
+                }
+            }
+            ob[i0] = v[0];  // ob is [RG][OUTCH]: item it sits at it
+            ob[i1] = u[0];
+        };
+        if constexpr (EVEN && !UNI && (RG * OUTCH) % 64 == 0) {
+#pragma unroll
+            for (int j = 0; j < RG * OUTCH / 64; j++) tree_pair(lane + 64 * j, lane + 64 * j + 32);
+        } else if constexpr (EVEN) {
             constexpr int ITEMS = RG * OUTCH;
 #pragma unroll
             for (int j = 0; j < (ITEMS + 31) / 32; j++) {
