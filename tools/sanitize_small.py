@@ -2,7 +2,7 @@
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth, paper_2106_00003_b200 as g
-sizes = [(8, 40), (12, 7), (64, 33), (256, 50), (1024, 20), (2047, 9), (4096, 5)]
+sizes = [(8, 40), (12, 7), (64, 33), (256, 50), (256, 64), (1024, 20), (1024, 64), (2047, 9), (2047, 32), (4096, 5), (4096, 16)]
 if len(sys.argv) > 1:
     sizes = [s for s in sizes if s[0] <= int(sys.argv[1])]
 for n, m in sizes:
