@@ -515,7 +515,11 @@ def main():
                          "traffic": traffic,
                          "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {peak_clock:.0f} MHz "
                                        "(max boost; DESIGN.md §5)",
-                         "flops_per_rotation_column": FLOPS_BWD, "ms_per_launch": ms_bwd},
+                         "flops_per_rotation_column": FLOPS_BWD, "ms_per_launch": ms_bwd,
+                         # the whole step (precompute + forward + backward) against the same peak, at
+                         # 6 + 16 algorithmic flops per rotation-column
+                         "step_achieved": (FLOPS_FWD + FLOPS_BWD) * N * m / (ms_step * 1e-3) / 1e12,
+                         "step_frac": (FLOPS_FWD + FLOPS_BWD) * N * m / (ms_step * 1e-3) / 1e12 / peak},
             "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd,
             "gpu_launches": 8 * args.steps,
             "clocks": clk,
