@@ -181,7 +181,7 @@ def test_strided_leading_dimension(g):
     assert rel(Y, oracle.apply(n, th, X.astype(np.float64))) <= TOL_Y
 
 
-@pytest.mark.parametrize("n", [8, 64, 255, 256, 1024, 2047, 4096])
+@pytest.mark.parametrize("n", [8, 48, 64, 255, 256, 1024, 1120, 2000, 2047, 4096])
 def test_fast_slab_path_bitwise(g, n):
     """The whole-slab fast load/store path (aligned rows, every column in range) and the general
     path (rows misaligned by one float, per-element checks) run the same arithmetic in the same
