@@ -37,6 +37,7 @@ M_TOTAL = 65536
 SEED = 0
 FP32_LANES_PER_SM = 128           # B200 SM: 4 SMSP x 32 FP32 lanes (B200_PROFILING.md / guide)
 FLOPS_FWD, FLOPS_BWD = 6, 16      # algorithmic flops per rotation-column
+SPIN_CYCLES = 4_000_000            # ~2 ms GPU spin ahead of short timed sequences (host enqueue hidden)
 
 
 def _env_int(k, d):
@@ -192,6 +193,10 @@ def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 409
         tf = tb = 0.0
         reps = 5
         for _ in range(reps):
+            # a GPU-side spin first, so the host has enqueued both calls before the GPU reaches
+            # them: the events then bracket device time only, not host enqueue gaps between
+            # sub-millisecond kernels
+            torch.cuda._sleep(SPIN_CYCLES)
             ev[0].record()
             g.build_U(th, n, out=U, ws=ws)
             ev[1].record()
@@ -226,6 +231,7 @@ def small_config_line(g, torch, synth, dev, n=256, m=4096, reps=20):
     tf = tb = 0.0
     for _ in range(reps):
         flush.fill_(1.0)
+        torch.cuda._sleep(SPIN_CYCLES)  # see ubuild_table
         ev[0].record()
         g.apply(th, X, out=Y, ws=ws)
         ev[1].record()
