@@ -177,7 +177,8 @@ def cpu_baseline(args, target_s: float = 12.0):
 
 def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 4096)):
     """Device ms of build_U (forward from U <- I, Alg. 2) and of its gradient (Alg. 3 via the replay
-    backward with Gamma = dL/dU) per n; mean of 5 after warm-up (the paper used 50 runs).
+    backward with Gamma = dL/dU) per n; mean of 10 back-to-back calls after a warm-up call (the
+    paper averaged 50 runs).
     n = 1120 and 2000 are the paper's CPU and GPU maxima."""
     table = {}
     for n in ns:
@@ -187,24 +188,26 @@ def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 409
         ws = g.workspace(g.OP_BACKWARD, n, n, dev)
         U = torch.empty(n, n, device=dev)
         dth = torch.empty(N, device=dev)
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         g.build_U(th, n, out=U, ws=ws)
         g.backward(th, U, G, ws=ws, recompute=False, dtheta=dth, want_dX=False)
-        tf = tb = 0.0
-        reps = 5
+        reps = 10
+        # `reps` calls back to back behind a GPU-side spin: the host has enqueued them all before
+        # the GPU reaches them, so the events bracket device time (sub-millisecond kernels would
+        # otherwise include host enqueue gaps), and the once-per-sequence shared-memory carveout
+        # switch after the spin is amortised over the calls
+        torch.cuda._sleep(SPIN_CYCLES)
+        ev[0].record()
         for _ in range(reps):
-            # a GPU-side spin first, so the host has enqueued both calls before the GPU reaches
-            # them: the events then bracket device time only, not host enqueue gaps between
-            # sub-millisecond kernels
-            torch.cuda._sleep(SPIN_CYCLES)
-            ev[0].record()
             g.build_U(th, n, out=U, ws=ws)
-            ev[1].record()
+        ev[1].record()
+        torch.cuda._sleep(SPIN_CYCLES)
+        ev[2].record()
+        for _ in range(reps):
             g.backward(th, U, G, ws=ws, recompute=False, dtheta=dth, want_dX=False)
-            ev[2].record()
-            torch.cuda.synchronize()
-            tf += ev[0].elapsed_time(ev[1])
-            tb += ev[1].elapsed_time(ev[2])
+        ev[3].record()
+        torch.cuda.synchronize()
+        tf, tb = ev[0].elapsed_time(ev[1]), ev[2].elapsed_time(ev[3])
         table[str(n)] = {"build_U_ms": round(tf / reps, 4), "grad_ms": round(tb / reps, 4)}
     return table
 
@@ -231,7 +234,6 @@ def small_config_line(g, torch, synth, dev, n=256, m=4096, reps=20):
     tf = tb = 0.0
     for _ in range(reps):
         flush.fill_(1.0)
-        torch.cuda._sleep(SPIN_CYCLES)  # see ubuild_table
         ev[0].record()
         g.apply(th, X, out=Y, ws=ws)
         ev[1].record()
