@@ -58,7 +58,10 @@ __host__ __device__ inline int64_t flat_of_bl(int r, int k, int n, int ne, int b
 #ifndef GK_BWD_WARPS
 #define GK_BWD_WARPS 8
 #endif
-constexpr int kNW = GK_BWD_WARPS;  // warps per CTA of the backward ring kernel
+constexpr int kNW = GK_BWD_WARPS;
+#ifndef RS_LC
+#define RS_LC 1  // reduce-scatter of the per-slot sums across column groups sharing a warp
+#endif  // warps per CTA of the backward ring kernel
 #ifndef GK_FWD_WARPS
 #define GK_FWD_WARPS 8
 #endif
@@ -393,6 +396,7 @@ __device__ __forceinline__ float2 cmul4(float2 z, float4 e) {
 }
 __device__ __forceinline__ float cmul4(float z, float4) { return z; }
 
+__host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -813,7 +817,30 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     }
                 }
                 if constexpr (GRAD) {
-                    if constexpr (LC > 1) {
+                    if constexpr (LC > 1 && !UNI && W / LC >= 4 && RS_LC) {
+                        // several column groups per warp share the slots: reduce-scatter over the
+                        // groups (log2 LC butterfly rounds, each lane keeps half of its live sums and
+                        // ships the other half) instead of an all-reduce of every slot -- W (LC-1)/LC
+                        // shuffles per lane and step instead of W log2 LC; group g ends up with the
+                        // W/LC slots at off(g) and stores them, the ring layout is unchanged
+                        int off = 0;
+                        unroll<ilog2(LC)>([&](auto jc) {
+                            constexpr int j = decltype(jc)::value;
+                            constexpr int h = W >> (j + 1);  // live sums after this round
+                            const bool hi = (lane >> (ilog2(LW) + j)) & 1;
+#pragma unroll
+                            for (int i = 0; i < h; i++) {
+                                const float send = hi ? acc[i] : acc[h + i];
+                                const float keep = hi ? acc[h + i] : acc[i];
+                                acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, LW << j);
+                            }
+                            if (hi) off += h;
+                        });
+#pragma unroll
+                        for (int k = 0; k < W / LC / 4; k++)
+                            ring_dst[(off / 4 + k) * LW + tl] =
+                                make_float4(acc[4 * k], acc[4 * k + 1], acc[4 * k + 2], acc[4 * k + 3]);
+                    } else if constexpr (LC > 1) {
 #pragma unroll
                         for (int q = 0; q < W; q++) {
 #pragma unroll
