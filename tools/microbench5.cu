@@ -53,8 +53,7 @@ __global__ void __launch_bounds__(256, 1) k(float *out, const float *__restrict_
                 x[j] = __ffma2_rn(make_float2(c[i], c[i]), y[j], x[j]);
             }
         }
-#pragma unroll
-        for (int i = 0; i < NCH; i++) c[i] = -c[i] * 0.999f;  // keep coefficients live and changing
+        // (coefficients are loop-invariant registers the compiler cannot fold: loaded from memory)
     }
     float s = 0;
 #pragma unroll
