@@ -14,6 +14,10 @@ per step).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
+With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py launches its own N ranks
+(torch.distributed.run, 127.0.0.1) and exits with their status; under a launcher it checks that
+WORLD_SIZE == --gpus.
+
 --impl reference times the fp64 CPU oracle (the only reference this paper has: it released no
 code) on the host cores, on a bounded column sample of the same workload.
 """
@@ -57,7 +61,8 @@ def parse():
     ap.add_argument("--m", type=int, default=M_TOTAL)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--ref-cols-per-step", type=int, default=128)
+    ap.add_argument("--ref-cols-per-step", type=int, default=0,
+                    help="reference arm columns per step (default 64 per oracle thread, so every core works)")
     ap.add_argument("--no-ubuild", action="store_true", help="skip the U-build ms vs n table")
     return ap.parse_args()
 
@@ -117,7 +122,10 @@ def run_reference(args, rank, world):
     import synth
     n, m = args.n, args.m
     N = n * (n - 1) // 2
-    cols = args.ref_cols_per_step
+    cores = oracle.num_threads()
+    # the oracle splits columns into 64-column blocks over its OpenMP threads: 64 per thread keeps
+    # every host core busy
+    cols = args.ref_cols_per_step or 64 * cores
     th = synth.theta(N, seed=SEED)
     times = []
     for s in range(args.warmup + args.steps):
@@ -132,7 +140,6 @@ def run_reference(args, rank, world):
             times.append(dt)
     t = sum(times) / len(times)
     value = N * cols / t
-    cores = oracle.num_threads()
     sample = f"{cols} of {m} columns per step (n={n}), fp64 oracle: Alg. 1 forward + taped reverse-mode backward"
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
@@ -172,7 +179,27 @@ def cpu_baseline(args, target_s: float = 12.0):
         t = run(cols)
     return {"value": N * cols / t, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
             "sample": f"first {cols} of {args.m} columns (n={n}): fp64 Alg. 1 forward + taped backward, "
-                      f"{t:.1f} s wall"}
+                      f"{t:.1f} s wall",
+            "single_core": single_core_rate(n, args.m)}
+
+
+def single_core_rate(n, m, cols=64):
+    """The same oracle on ONE host thread (OMP_NUM_THREADS=1, a fresh process), on `cols` columns."""
+    code = ("import time,sys,numpy as np; sys.path.insert(0, %r); import oracle, synth\n"
+            "n,m,c=%d,%d,%d; th=synth.theta(n*(n-1)//2, seed=%d)\n"
+            "X=synth.normal_matrix(n,m,%d,synth.TID_X,0,c).astype(np.float64)\n"
+            "dY=synth.normal_matrix(n,m,%d,synth.TID_DY,0,c).astype(np.float64)\n"
+            "t0=time.perf_counter(); oracle.apply(n,th,X); oracle.backward(n,th,X,dY)\n"
+            "print(oracle.num_threads(), time.perf_counter()-t0)" % (ROOT, n, m, cols, SEED, SEED, SEED))
+    try:
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                           env=dict(os.environ, OMP_NUM_THREADS="1"))
+        thr, t = r.stdout.split()[-2:]
+        N = n * (n - 1) // 2
+        return {"value": N * cols / float(t), "unit": UNIT, "cores": int(thr),
+                "sample": f"first {cols} columns (n={n}), {float(t):.2f} s"}
+    except Exception as e:  # the single-core figure is context only
+        return {"error": repr(e)[:200]}
 
 
 def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 4096)):
@@ -191,7 +218,7 @@ def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 409
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         g.build_U(th, n, out=U, ws=ws)
         g.backward(th, U, G, ws=ws, recompute=False, dtheta=dth, want_dX=False)
-        reps = 10
+        reps = 50
         # `reps` calls back to back behind a GPU-side spin: the host has enqueued them all before
         # the GPU reaches them, so the events bracket device time (sub-millisecond kernels would
         # otherwise include host enqueue gaps), and the once-per-sequence shared-memory carveout
@@ -217,7 +244,7 @@ def ubuild_table(g, torch, synth, dev, ns=(256, 512, 1024, 1120, 2000, 2048, 409
 UFLOPS_FWD, UFLOPS_BWD = 18, 64
 
 
-def small_config_line(g, torch, synth, dev, n=256, m=4096, reps=20):
+def small_config_line(g, torch, synth, dev, n=256, m=4096, reps=50):
     """BASELINE config C2 (n=256, m=4096, 1 GPU): device ms of apply + backward (dX, dtheta), mean of
     `reps` after warm-up, L2 flushed before each; latency-bound (28 columns per SM)."""
     N = n * (n - 1) // 2
@@ -325,6 +352,35 @@ def unitary_line(g, torch, synth, dev, peak_tflops, n=1024, m=32768, reps=5):
             "flops_per_complex_rotation_column": {"fwd": UFLOPS_FWD, "bwd": UFLOPS_BWD}}
 
 
+def step_reps(g, torch, theta, X, dY, n, reps=50, m_cols=None):
+    """The paper's protocol ("averaged over 50 runs"): `reps` timed steps (precompute +
+    forward + backward), each after an L2 flush, CUDA events on the stream; mean / std / min ms.
+    m_cols < m times the step on the first m_cols columns (one rank's shard of a G-GPU run)."""
+    dev = X.device
+    if m_cols is not None:
+        X, dY = X[:, :m_cols].contiguous(), dY[:, :m_cols].contiguous()
+    m = X.shape[1]
+    ws = g.workspace(g.OP_BACKWARD, n, m, dev)
+    Y, dX, dth = torch.empty_like(X), torch.empty_like(X), torch.empty_like(theta)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+
+    def step():
+        g.apply(theta, X, out=Y, ws=ws)
+        g.backward(theta, Y, dY, ws=ws, recompute=False, dtheta=dth, dX=dX)
+    for _ in range(3):
+        step()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for k in range(reps):
+        flush.fill_(float(k))
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    t = [a.elapsed_time(b) for a, b in ev]
+    return {"reps": reps, "m": m, "mean_ms": statistics.mean(t), "std_ms": statistics.stdev(t), "min_ms": min(t),
+            "max_ms": max(t)}
+
+
 def _measured_peak(key, default):
     """A number from the driver-written MEASURED_PEAKS.json, else the stated fallback."""
     try:
@@ -372,11 +428,28 @@ def gemm_path_line(g, torch, theta, X, dY, n, m, ring_ms, tf32_peak, reps=10):
 
 
 # ------------------------------------------------------------------ our arm
+def self_launch(args):
+    """--gpus N > 1 without a launcher: run N ranks under torch.distributed.run (one node,
+    127.0.0.1, a free port) and return their exit status."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -453,6 +526,8 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    step_stats = {"mean_ms": statistics.mean(step_ms), "min_ms": min(step_ms), "max_ms": max(step_ms),
+                  "std_ms": statistics.stdev(step_ms) if len(step_ms) > 1 else 0.0}
     t_rank = torch.tensor([sum(step_ms) / len(step_ms), sum(bwd_ms) / len(bwd_ms)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t_rank, op=dist.ReduceOp.MAX)
@@ -528,7 +603,7 @@ def main():
                          # 6 + 16 algorithmic flops per rotation-column
                          "step_achieved": (FLOPS_FWD + FLOPS_BWD) * N * m / (ms_step * 1e-3) / 1e12,
                          "step_frac": (FLOPS_FWD + FLOPS_BWD) * N * m / (ms_step * 1e-3) / 1e12 / peak},
-            "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd,
+            "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd, "step_ms_stats_rank0": step_stats,
             "gpu_launches": 8 * args.steps,
             "clocks": clk,
         }
@@ -537,6 +612,15 @@ def main():
         if ubuild:
             out["ubuild_ms_vs_n"] = ubuild
         if world == 1 and not args.no_ubuild:
+            out["paper_protocol_50"] = step_reps(g, torch, theta, X, dY, n)
+            # one rank's share of a G-GPU run of the same C3 step, timed here: the per-rank device
+            # time at G GPUs is this plus the dtheta all_reduce
+            scan = {}
+            for G in (2, 4, 8):
+                r = step_reps(g, torch, theta, X, dY, n, reps=20, m_cols=m // G)
+                scan[str(G)] = {"m_per_rank": m // G, "mean_ms": r["mean_ms"], "min_ms": r["min_ms"],
+                                "speedup_no_comm": out["paper_protocol_50"]["mean_ms"] / r["mean_ms"]}
+            out["shard_scan"] = scan
             out["c2"] = small_config_line(g, torch, synth, dev)
             out["c5_shard"] = c5_shard_line(g, torch, synth, dev)
             out["unitary"] = unitary_line(g, torch, synth, dev, peak)

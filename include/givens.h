@@ -23,19 +23,26 @@
  *          length; X, Y, dY, dX are n x m, U is n x n. All data pointers are DEVICE pointers
  *          (cudaMalloc / torch CUDA tensors), caller-owned; nothing is retained after return.
  * ws       device workspace of at least givens_workspace_bytes(op, n, m) bytes, 256-byte
- *          aligned, caller-owned; it may be reused across calls on the same stream. For
- *          givens_backward, ws must be the SAME workspace a preceding givens_apply /
- *          givens_build_U call with the same (n, theta, mask) filled, unless
- *          GIVENS_FLAG_RECOMPUTE is passed (then the coefficient tables are rebuilt).
+ *          aligned, caller-owned; it may be reused across calls on the same stream. ws = NULL
+ *          is allowed: the call then allocates its workspace stream-ordered on `stream`
+ *          (cudaMallocAsync from the device's default pool) and frees it (cudaFreeAsync) before
+ *          returning; GIVENS_ENOMEM if that allocation fails. Every call is self-contained by
+ *          default: it computes its coefficient tables from theta/mask itself. Only
+ *          givens_backward with GIVENS_FLAG_REUSE_TABLES consumes the tables a preceding
+ *          givens_apply / givens_build_U (same stream) left in ws; the library remembers, per
+ *          workspace address, the (device, n, theta, mask, perm, reflect_col) pointers the tables
+ *          were built from and refuses a mismatch with GIVENS_EINVAL (it cannot see a theta
+ *          rewritten in place at the same address: do not pass the flag then).
  * stream   cudaStream_t (as void*), NULL = legacy default stream. Every call is
  *          stream-ordered and asynchronous: it enqueues kernels and returns; results are
- *          visible after the stream is synchronised. No call allocates device memory.
+ *          visible after the stream is synchronised. No call allocates device memory unless
+ *          ws == NULL.
  * empty    m = 0 is valid: X, Y, dY, dX may then be NULL; dtheta (dphi) is written as zeros.
  * errors   0 on success; negative givens_status_t otherwise, with a thread-local message
  *          from givens_last_error(). Parameter errors are detected before anything is
  *          enqueued. Asynchronous CUDA faults surface at the next synchronising call.
- * threads  all functions are thread-safe (no global mutable state besides the thread-local
- *          error string and a per-device attribute cache).
+ * threads  all functions are thread-safe (global state: the thread-local error string, a
+ *          per-device attribute cache and the mutex-guarded workspace table tags).
  */
 #ifndef GIVENS_H_
 #define GIVENS_H_
@@ -51,12 +58,16 @@ typedef enum {
     GIVENS_OK = 0,
     GIVENS_EINVAL = -1,       /* bad argument (size, pointer, leading dimension, workspace) */
     GIVENS_ECUDA = -2,        /* a CUDA launch / attribute call failed */
-    GIVENS_EUNSUPPORTED = -3  /* valid arguments but no kernel configuration for this n yet */
+    GIVENS_EUNSUPPORTED = -3, /* valid arguments but no kernel configuration for this n yet */
+    GIVENS_ENOMEM = -4        /* ws == NULL and the stream-ordered workspace allocation failed */
 } givens_status_t;
 
 enum { GIVENS_OP_APPLY = 0, GIVENS_OP_BUILD_U = 1, GIVENS_OP_BACKWARD = 2,
        GIVENS_OP_U_APPLY = 3, GIVENS_OP_U_BUILD_U = 4, GIVENS_OP_U_BACKWARD = 5 };
-enum { GIVENS_FLAG_RECOMPUTE = 1 };
+/* backward flags: GIVENS_FLAG_RECOMPUTE (the default behaviour, accepted for clarity) rebuilds the
+ * coefficient tables from theta/mask; GIVENS_FLAG_REUSE_TABLES reads those a forward call left in
+ * ws (checked against the workspace's tag, see `ws` above). */
+enum { GIVENS_FLAG_RECOMPUTE = 1, GIVENS_FLAG_REUSE_TABLES = 2 };
 
 /* Thread-local description of the last failure ("" if none). */
 const char *givens_last_error(void);
@@ -109,7 +120,8 @@ int givens_build_U(int32_t n, const float *theta, const uint8_t *mask, float *U,
  * each dtheta_e is reduced over the m columns with a fixed-order, atomic-free two-stage sum
  * (PAPER.md:768-781), so the result is bitwise deterministic for a given (n, m, device).
  * With X = I, Y = U, dY = Gamma this is the paper's Algorithm 3.
- * flags: GIVENS_FLAG_RECOMPUTE rebuilds the coefficient tables from theta/mask.
+ * flags: 0 (or GIVENS_FLAG_RECOMPUTE) builds the coefficient tables from theta/mask;
+ * GIVENS_FLAG_REUSE_TABLES reuses a forward's tables in ws (EINVAL if ws holds none for these inputs).
  */
 int givens_backward(int32_t n, int64_t m, const float *theta, const uint8_t *mask,
                     const float *Y, int64_t ldy, const float *dY, int64_t lddy,
@@ -172,8 +184,8 @@ int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi
  *              U' = U diag(.., -1 at c, ..). apply: Y = U' X; transpose: U'^T X; backward:
  *              dtheta of L(U' X), dX = U'^T dY. Costs nothing in the kernels (it is one more
  *              sign in the per-row sign bookkeeping).
- * A givens_backward_ex without GIVENS_FLAG_RECOMPUTE must use the workspace of a forward call
- * with the same (n, theta, mask, perm, reflect_col). The calls without _ex are the _ex calls
+ * A givens_backward_ex with GIVENS_FLAG_REUSE_TABLES must use the workspace of a forward call
+ * with the same (n, theta, mask, perm, reflect_col) (checked). The calls without _ex are the _ex calls
  * with perm = NULL, reflect_col = -1.
  * ------------------------------------------------------------------------------------------ */
 
@@ -216,7 +228,8 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
  * givens_gemm_workspace_bytes(n, m) (it holds U and the hi/lo splits: ~4 n m floats), the GEMMs
  * run in cuBLAS (libcublas.so.12, loaded at first use; GIVENS_EUNSUPPORTED if absent; cuBLAS
  * allocates its own handle/workspace once per thread and device), and nothing may alias.
- * givens_gemm_backward without GIVENS_FLAG_RECOMPUTE reuses the U a givens_gemm_apply left in ws.
+ * givens_gemm_backward with GIVENS_FLAG_REUSE_TABLES reuses the U a givens_gemm_apply with the same
+ * inputs left in ws (checked as above); ws = NULL allocates stream-ordered as above.
  * ------------------------------------------------------------------------------------------ */
 size_t givens_gemm_workspace_bytes(int32_t n, int64_t m);
 int givens_gemm_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,

@@ -11,10 +11,10 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgivens.so")
 
-OK, EINVAL, ECUDA, EUNSUPPORTED = 0, -1, -2, -3
+OK, EINVAL, ECUDA, EUNSUPPORTED, ENOMEM = 0, -1, -2, -3, -4
 OP_APPLY, OP_BUILD_U, OP_BACKWARD = 0, 1, 2
 OP_U_APPLY, OP_U_BUILD_U, OP_U_BACKWARD = 3, 4, 5
-FLAG_RECOMPUTE = 1
+FLAG_RECOMPUTE, FLAG_REUSE_TABLES = 1, 2
 
 EXPORTS = [
     "givens_last_error", "givens_version", "givens_num_angles", "givens_supported",

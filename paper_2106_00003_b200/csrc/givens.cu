@@ -24,6 +24,7 @@
 #include <utility>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/givens.h"
 #include "common.cuh"
@@ -163,13 +164,78 @@ int launch_mode(const Cfg &c, int mode, int64_t m) {
     return (slabs < dev_sms() && slabs_n > slabs) ? (mode | M_NARROW) : mode;
 }
 
+// the generic backward keeps a private [vals][2S][S] fp32 partial per CTA; its grid is capped so
+// that the partials stay within this budget (n = 8192 would otherwise need 1184 x 134 MB)
+constexpr size_t kGenericPartialBudget = (size_t)4 << 30;
+
 int64_t grid_for(const Cfg &c, int mode0, int64_t m) {
     const int mode = launch_mode(c, mode0, m);
     int64_t slabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
     int64_t per_sm = c.fast ? 1 : 8;
     int64_t g = std::min<int64_t>(slabs, (int64_t)dev_sms() * per_sm);
+    if (!c.fast && (mode & 3) == M_BWD) {
+        const size_t per_cta = (size_t)2 * c.S * c.S * 4 * ((mode & M_UNI) ? 2 : 1);
+        g = std::min<int64_t>(g, (int64_t)std::max<size_t>(1, kGenericPartialBudget / per_cta));
+    }
     return std::max<int64_t>(g, 1);
 }
+
+// ---- coefficient-table tags. A backward with GIVENS_FLAG_REUSE_TABLES consumes the tables a
+// forward call left in the workspace; the host remembers, per workspace address, what the last
+// precompute into it was built from, and a reuse whose (device, n, configuration, theta, phi,
+// mask, perm, reflect_col) differ is refused with GIVENS_EINVAL instead of silently reading stale
+// tables. (Pointers, not contents: a caller that rewrites theta in place between the forward and
+// a reusing backward must not pass the flag.)
+struct TableTag {
+    int dev, n, W, L, uni, refl;
+    const void *theta, *phi, *mask, *perm;
+    bool operator==(const TableTag &o) const {
+        return dev == o.dev && n == o.n && W == o.W && L == o.L && uni == o.uni && refl == o.refl &&
+               theta == o.theta && phi == o.phi && mask == o.mask && perm == o.perm;
+    }
+};
+std::mutex g_tag_mu;
+std::unordered_map<const void *, TableTag> g_tags;
+
+TableTag make_tag(const Cfg &c, int n, const float *theta, const float *phi, const uint8_t *mask,
+                  const int32_t *perm, int refl) {
+    int d = -1;
+    cudaGetDevice(&d);
+    return TableTag{d, n, c.W, c.L, phi ? 1 : 0, refl, theta, phi, mask, perm};
+}
+void tag_tables(const void *ws, const TableTag &t) {
+    std::lock_guard<std::mutex> g(g_tag_mu);
+    g_tags[ws] = t;
+}
+void untag_tables(const void *ws) {
+    std::lock_guard<std::mutex> g(g_tag_mu);
+    g_tags.erase(ws);
+}
+int check_tables(const void *ws, const TableTag &want) {
+    if (!ws) return fail(GIVENS_EINVAL, "GIVENS_FLAG_REUSE_TABLES needs the forward's workspace (ws is NULL)");
+    std::lock_guard<std::mutex> g(g_tag_mu);
+    auto it = g_tags.find(ws);
+    if (it == g_tags.end())
+        return fail(GIVENS_EINVAL, "GIVENS_FLAG_REUSE_TABLES: no forward call filled this workspace");
+    if (!(it->second == want))
+        return fail(GIVENS_EINVAL, "GIVENS_FLAG_REUSE_TABLES: the workspace tables were built for a different "
+                                   "(n, theta, phi, mask, perm, reflect_col) or device");
+    return 0;
+}
+
+// ---- ws == NULL: a stream-ordered workspace for this call (cudaMallocAsync / cudaFreeAsync on the
+// call's stream, from the device's default memory pool)
+struct AutoWs {
+    void *p = nullptr;
+    cudaStream_t st = nullptr;
+    int get(void *&ws, size_t &bytes, size_t need, cudaStream_t s);
+    ~AutoWs() {
+        if (p) {
+            untag_tables(p);
+            cudaFreeAsync(p, st);
+        }
+    }
+};
 
 struct WsLayout {
     size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, segx, lay, partial, scratch, total;
@@ -237,6 +303,19 @@ __global__ void k_layout(int n, int ne, const int32_t *__restrict__ perm, int re
     }
 }
 
+// theta -> the angle phi in [-pi/2, pi/2] with R(theta) = (-1)^flip R(phi). theta is
+// any real (theta in R^N): it is first reduced to [-pi, pi] by the exact fp64
+// remainder modulo 2 pi (R is 2 pi-periodic), then flipped by pi when |.| > pi/2, so the shear
+// coefficient tan(phi/2) stays in [-1, 1] for every theta. k_flip, k_coef and k_coef_u all use it,
+// so the flip bits and the table agree.
+__device__ __forceinline__ double reduce_angle(double th, int *flip) {
+    double r = remainder(th, 6.283185307179586);
+    const int fl = fabs(r) > 1.5707963267948966 ? 1 : 0;
+    if (fl) r -= copysign(3.141592653589793, r);
+    if (flip) *flip = fl;
+    return r;
+}
+
 // (1) flip bit per (block, slot): |theta| > pi/2 => R(theta) = -R(theta -/+ pi).
 __global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uint8_t *__restrict__ mask,
                        const int32_t *__restrict__ lay, uint8_t *__restrict__ flip) {
@@ -246,7 +325,11 @@ __global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uin
     int r = (int)(idx / S), k = (int)(idx % S);
     int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
     uint8_t fl = 0;
-    if (f >= 0 && (!mask || mask[f])) fl = fabs((double)theta[f]) > 1.5707963267948966 ? 1 : 0;
+    if (f >= 0 && (!mask || mask[f])) {
+        int fb;
+        reduce_angle((double)theta[f], &fb);
+        fl = (uint8_t)fb;
+    }
     flip[idx] = fl;
 }
 
@@ -319,8 +402,7 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
     int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
     bool active = f >= 0 && (!mask || mask[f]);
     double th = active ? (double)theta[f] : 0.0;
-    double phi = th;
-    if (fabs(th) > 1.5707963267948966) phi = th - copysign(3.141592653589793, th);
+    const double phi = reduce_angle(th, nullptr);
     int neg = (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) ^ (lay[a] > lay[b] ? 1 : 0);
     double tq = tan(0.5 * phi), sq = sin(phi);
     if (neg) { tq = -tq; sq = -sq; }
@@ -360,8 +442,7 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
     int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
     bool active = f >= 0 && (!mask || mask[f]);
     double th = active ? (double)theta[f] : 0.0, pv = active ? (double)phi[f] : 0.0;
-    double thr = th;
-    if (fabs(th) > 1.5707963267948966) thr = th - copysign(3.141592653589793, th);
+    const double thr = reduce_angle(th, nullptr);
     float pc = (float)cos(pv), ps = (float)sin(pv);
     bool top_is_i = lay[a] < lay[b];
     phr[pos_ph] = top_is_i ? make_float4(pc, ps, 1.f, 0.f) : make_float4(1.f, 0.f, pc, ps);
@@ -744,6 +825,7 @@ constexpr Lay kNoLay{nullptr, -1};
 int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask, uint8_t *ws, const WsLayout &L,
                    cudaStream_t st, const float *phi = nullptr, Lay lo = kNoLay) {
     int64_t RS = (int64_t)c.R * c.S;
+    untag_tables(ws);  // partially rebuilt tables must not pass for the old ones if a launch fails
     int32_t *lay = reinterpret_cast<int32_t *>(ws + L.lay);
     k_layout<<<1, 1024, 0, st>>>(n, c.ne, lo.perm, lo.refl, lay);
     CUDA_TRY(cudaGetLastError());
@@ -770,14 +852,31 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
                                                                 reinterpret_cast<float2 *>(ws + L.coef_ab));
         CUDA_TRY(cudaGetLastError());
     }
+    tag_tables(ws, make_tag(c, n, theta, phi, mask, lo.perm, lo.refl));
     return 0;
 }
 
+int AutoWs::get(void *&ws, size_t &bytes, size_t need, cudaStream_t s) {
+    if (ws) return 0;
+    cudaError_t e = cudaMallocAsync(&p, need ? need : 256, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        p = nullptr;
+        return fail(e == cudaErrorMemoryAllocation ? GIVENS_ENOMEM : GIVENS_ECUDA,
+                    "cudaMallocAsync of a %zu-byte workspace: %s", need, cudaGetErrorString(e));
+    }
+    st = s;
+    ws = p;
+    bytes = need;
+    return 0;
+}
+
+// ws may be NULL (a stream-ordered workspace is then allocated for the call, AutoWs)
 int check_common(int32_t n, int64_t m, const void *ws, size_t ws_bytes, int op) {
     if (n < 2) return fail(GIVENS_EINVAL, "n must be >= 2 (got %d)", n);
     if (n > 32768) return fail(GIVENS_EINVAL, "n must be <= 32768 (got %d)", n);
     if (m < 0) return fail(GIVENS_EINVAL, "m must be >= 0");
-    if (!ws) return fail(GIVENS_EINVAL, "workspace is NULL");
+    if (!ws) return 0;
     if (((uintptr_t)ws) % 256) return fail(GIVENS_EINVAL, "workspace must be 256-byte aligned");
     size_t need = givens_workspace_bytes(op, n, m);
     if (ws_bytes < need) return fail(GIVENS_EINVAL, "workspace too small: %zu < %zu", ws_bytes, need);
@@ -929,6 +1028,8 @@ int givens_u_apply_ex(int32_t n, int64_t m, const float *theta, const float *phi
     Cfg c = make_cfg_u(n);
     WsLayout L = ws_layout(c, GIVENS_OP_U_APPLY, m);
     cudaStream_t st = (cudaStream_t)stream;
+    AutoWs aw;
+    if ((rc = aw.get(ws, ws_bytes, L.total, st))) return rc;
     uint8_t *w = (uint8_t *)ws;
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
     // a complex column is two interleaved real columns
@@ -946,6 +1047,8 @@ int givens_u_build_U_ex(int32_t n, const float *theta, const float *phi, const u
     Cfg c = make_cfg_u(n);
     WsLayout L = ws_layout(c, GIVENS_OP_U_BUILD_U, n);
     cudaStream_t st = (cudaStream_t)stream;
+    AutoWs aw;
+    if ((rc = aw.get(ws, ws_bytes, L.total, st))) return rc;
     uint8_t *w = (uint8_t *)ws;
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
     return run_apply_mode(M_BUILDU | M_UNI, n, 2 * (int64_t)n, nullptr, 0, nullptr, 0, U, 2 * ldu, w, L, c, st, perm);
@@ -964,8 +1067,13 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
     Cfg c = make_cfg_u(n);
     WsLayout L = ws_layout(c, GIVENS_OP_U_BACKWARD, m);
     cudaStream_t st = (cudaStream_t)stream;
+    if (flags & GIVENS_FLAG_REUSE_TABLES) {
+        if ((rc = check_tables(ws, make_tag(c, n, theta, phi, mask, perm, reflect_col)))) return rc;
+    }
+    AutoWs aw;
+    if ((rc = aw.get(ws, ws_bytes, L.total, st))) return rc;
     uint8_t *w = (uint8_t *)ws;
-    if (flags & GIVENS_FLAG_RECOMPUTE) {
+    if (!(flags & GIVENS_FLAG_REUSE_TABLES)) {
         if ((rc = run_precompute(c, n, theta, mask, w, L, st, phi, Lay{perm, reflect_col}))) return rc;
     }
     int64_t N = givens_num_angles(n);
@@ -996,6 +1104,8 @@ int givens_apply_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     Cfg c = make_cfg(n);
     WsLayout L = ws_layout(c, GIVENS_OP_APPLY, m);
     cudaStream_t st = (cudaStream_t)stream;
+    AutoWs aw;
+    if ((rc = aw.get(ws, ws_bytes, L.total, st))) return rc;
     uint8_t *w = (uint8_t *)ws;
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
     return run_apply_mode(transpose ? M_TRANS : M_FWD, n, m, X, ldx, nullptr, 0, Y, ldy, w, L, c, st, perm);
@@ -1012,6 +1122,8 @@ int givens_build_U_ex(int32_t n, const float *theta, const uint8_t *mask, float 
     Cfg c = make_cfg(n);
     WsLayout L = ws_layout(c, GIVENS_OP_BUILD_U, n);
     cudaStream_t st = (cudaStream_t)stream;
+    AutoWs aw;
+    if ((rc = aw.get(ws, ws_bytes, L.total, st))) return rc;
     uint8_t *w = (uint8_t *)ws;
     if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
     return run_apply_mode(M_BUILDU, n, n, nullptr, 0, nullptr, 0, U, ldu, w, L, c, st, perm);
@@ -1029,8 +1141,13 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
     Cfg c = make_cfg(n);
     WsLayout L = ws_layout(c, GIVENS_OP_BACKWARD, m);
     cudaStream_t st = (cudaStream_t)stream;
+    if (flags & GIVENS_FLAG_REUSE_TABLES) {
+        if ((rc = check_tables(ws, make_tag(c, n, theta, nullptr, mask, perm, reflect_col)))) return rc;
+    }
+    AutoWs aw;
+    if ((rc = aw.get(ws, ws_bytes, L.total, st))) return rc;
     uint8_t *w = (uint8_t *)ws;
-    if (flags & GIVENS_FLAG_RECOMPUTE) {
+    if (!(flags & GIVENS_FLAG_REUSE_TABLES)) {
         if ((rc = run_precompute(c, n, theta, mask, w, L, st, nullptr, Lay{perm, reflect_col}))) return rc;
     }
     int64_t N = givens_num_angles(n);

@@ -21,6 +21,12 @@ def allreduce_dtheta(dtheta: torch.Tensor, group=None, deterministic: bool = Fal
     and sums them in rank order (bitwise reproducible for a fixed world size)."""
     if not dist.is_available() or not dist.is_initialized() or dist.get_world_size(group) == 1:
         return dtheta
+    if dtheta.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo (CPU tests, or several ranks sharing one GPU) reduces host tensors: stage through the host
+        host = dtheta.cpu()
+        allreduce_dtheta(host, group=group, deterministic=deterministic)
+        dtheta.copy_(host)
+        return dtheta
     if not deterministic:
         dist.all_reduce(dtheta, op=dist.ReduceOp.SUM, group=group)
         return dtheta

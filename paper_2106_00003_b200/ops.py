@@ -6,12 +6,14 @@ libgivens.so's sm_100a kernels. These wrappers only check shapes/dtypes and mars
 from __future__ import annotations
 
 import ctypes
+import functools
+import itertools
 
 import numpy as np
 import torch
 
 from . import _lib
-from ._lib import (FLAG_RECOMPUTE, OP_APPLY, OP_BACKWARD, OP_BUILD_U, OP_U_APPLY, OP_U_BACKWARD, OP_U_BUILD_U,
+from ._lib import (FLAG_RECOMPUTE, FLAG_REUSE_TABLES, OP_APPLY, OP_BACKWARD, OP_BUILD_U, OP_U_APPLY, OP_U_BACKWARD, OP_U_BUILD_U,
                    check, lib)
 
 
@@ -100,7 +102,10 @@ def workspace_bytes(op: int, n: int, m: int) -> int:
 
 
 def workspace(op: int, n: int, m: int, device=None) -> torch.Tensor:
-    nb = workspace_bytes(op, n, m)
+    """A workspace for op on `device` (its size depends on that device's SM count)."""
+    device = torch.device(device or "cuda")
+    with torch.cuda.device(device):
+        nb = workspace_bytes(op, n, m)
     if nb == 0:
         raise ValueError(f"bad workspace query op={op} n={n} m={m}")
     return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
@@ -120,6 +125,30 @@ def _check_matrix(name, t, n):
                          f"(got {tuple(t.shape)} {t.dtype} {t.device} strides {t.stride()})")
 
 
+def _same_shape(name, t, ref):
+    if tuple(t.shape) != tuple(ref.shape):
+        raise ValueError(f"{name} must have shape {tuple(ref.shape)} (got {tuple(t.shape)})")
+
+
+def _on_device(fn):
+    """Run an op with the device of its CUDA tensor arguments current (the library launches on, and
+    sizes grids for, the current device), and refuse tensors on different devices."""
+    @functools.wraps(fn)
+    def wrapper(*args, **kwargs):
+        devs = {t.device for t in itertools.chain(args, kwargs.values()) if isinstance(t, torch.Tensor) and t.is_cuda}
+        if len(devs) > 1:
+            raise ValueError(f"{fn.__name__}: tensors on different devices {sorted(map(str, devs))}")
+        if not devs:
+            return fn(*args, **kwargs)
+        with torch.cuda.device(devs.pop()):
+            return fn(*args, **kwargs)
+    return wrapper
+
+
+def _flags(recompute: bool) -> int:
+    return FLAG_RECOMPUTE if recompute else FLAG_REUSE_TABLES
+
+
 def _check_theta(theta, mask, n):
     N = num_angles(n)
     if not (theta.is_cuda and theta.dtype == torch.float32 and theta.is_contiguous() and theta.numel() == N):
@@ -129,6 +158,7 @@ def _check_theta(theta, mask, n):
         raise ValueError(f"mask must be a contiguous CUDA uint8 tensor of {N} entries")
 
 
+@_on_device
 def apply(theta: torch.Tensor, X: torch.Tensor, mask: torch.Tensor | None = None, transpose: bool = False,
           out: torch.Tensor | None = None, ws: torch.Tensor | None = None, layout: Layout | None = None) -> torch.Tensor:
     """Y = U(theta) X (or U^T X): Algorithm 2 on the columns of X."""
@@ -137,6 +167,7 @@ def apply(theta: torch.Tensor, X: torch.Tensor, mask: torch.Tensor | None = None
     _check_theta(theta, mask, n)
     Y = torch.empty_like(X) if out is None else out
     _check_matrix("out", Y, n)
+    _same_shape("out", Y, X)
     if ws is None:
         ws = workspace(OP_APPLY, n, m, X.device)
     check(lib().givens_apply_ex(n, m, _ptr(theta), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y), Y.stride(0),
@@ -145,12 +176,15 @@ def apply(theta: torch.Tensor, X: torch.Tensor, mask: torch.Tensor | None = None
     return Y
 
 
+@_on_device
 def build_U(theta: torch.Tensor, n: int, mask: torch.Tensor | None = None, out: torch.Tensor | None = None,
             ws: torch.Tensor | None = None, layout: Layout | None = None) -> torch.Tensor:
     """U = U(theta) (Algorithm 2 from U <- I_n)."""
     _check_theta(theta, mask, n)
     U = torch.empty((n, n), dtype=torch.float32, device=theta.device) if out is None else out
     _check_matrix("U", U, n)
+    if U.shape[1] != n:
+        raise ValueError(f"U must be [{n}, {n}] (got {tuple(U.shape)})")
     if ws is None:
         ws = workspace(OP_BUILD_U, n, n, theta.device)
     check(lib().givens_build_U_ex(n, _ptr(theta), _ptr(mask), _ptr(U), U.stride(0), *_lay(layout, n, theta.device),
@@ -158,16 +192,19 @@ def build_U(theta: torch.Tensor, n: int, mask: torch.Tensor | None = None, out: 
     return U
 
 
+@_on_device
 def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch.Tensor | None = None,
              want_dX: bool = True, ws: torch.Tensor | None = None, recompute: bool = True,
              dtheta: torch.Tensor | None = None, dX: torch.Tensor | None = None, layout: Layout | None = None):
     """(dtheta, dX) for Y = U(theta) X given Y and dY (replay backward, §4).
 
     recompute=False reuses the coefficient tables a preceding apply/build_U left in `ws`
-    (ws must then be a backward-sized workspace that the forward used)."""
+    (ws must then be a backward-sized workspace that the forward used with the same theta, mask
+    and layout; the library checks this and raises otherwise)."""
     n, m = Y.shape
     _check_matrix("Y", Y, n)
     _check_matrix("dY", dY, n)
+    _same_shape("dY", dY, Y)
     _check_theta(theta, mask, n)
     if ws is None:
         ws = workspace(OP_BACKWARD, n, m, Y.device)
@@ -178,9 +215,10 @@ def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch
         dX = torch.empty_like(dY)
     if dX is not None:
         _check_matrix("dX", dX, n)
+        _same_shape("dX", dX, dY)
     check(lib().givens_backward_ex(n, m, _ptr(theta), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY), dY.stride(0),
                                    _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
-                                   FLAG_RECOMPUTE if recompute else 0, *_lay(layout, n, Y.device), _ptr(ws),
+                                   _flags(recompute), *_lay(layout, n, Y.device), _ptr(ws),
                                    ws.numel(), _stream(Y.device)))
     return dtheta, dX
 
@@ -188,12 +226,15 @@ def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch
 # ---------------------------------------------------------------- GEMM path
 
 def gemm_workspace(n: int, m: int, device=None) -> torch.Tensor:
-    nb = int(lib().givens_gemm_workspace_bytes(n, m))
+    device = torch.device(device or "cuda")
+    with torch.cuda.device(device):
+        nb = int(lib().givens_gemm_workspace_bytes(n, m))
     if nb == 0:
         raise ValueError(f"bad GEMM workspace query n={n} m={m}")
     return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
 
 
+@_on_device
 def gemm_apply(theta, X, mask=None, transpose: bool = False, out=None, ws=None, layout: Layout | None = None):
     """Y = U(theta) X via U-build (register ring) + a 3xTF32 tensor-core GEMM."""
     n, m = X.shape
@@ -201,6 +242,7 @@ def gemm_apply(theta, X, mask=None, transpose: bool = False, out=None, ws=None, 
     _check_theta(theta, mask, n)
     Y = torch.empty_like(X) if out is None else out
     _check_matrix("out", Y, n)
+    _same_shape("out", Y, X)
     if ws is None:
         ws = gemm_workspace(n, m, X.device)
     check(lib().givens_gemm_apply(n, m, _ptr(theta), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y), Y.stride(0),
@@ -209,12 +251,14 @@ def gemm_apply(theta, X, mask=None, transpose: bool = False, out=None, ws=None, 
     return Y
 
 
+@_on_device
 def gemm_backward(theta, Y, dY, mask=None, want_dX: bool = True, ws=None, recompute: bool = True,
                   dtheta=None, dX=None, layout: Layout | None = None):
     """(dtheta, dX) via dX = U^T dY, Gamma = (dY Y^T) U (3xTF32 GEMMs) and Alg. 3 on Gamma."""
     n, m = Y.shape
     _check_matrix("Y", Y, n)
     _check_matrix("dY", dY, n)
+    _same_shape("dY", dY, Y)
     _check_theta(theta, mask, n)
     if ws is None:
         ws = gemm_workspace(n, m, Y.device)
@@ -223,9 +267,12 @@ def gemm_backward(theta, Y, dY, mask=None, want_dX: bool = True, ws=None, recomp
         dtheta = torch.empty(num_angles(n), dtype=torch.float32, device=Y.device)
     if want_dX and dX is None:
         dX = torch.empty_like(dY)
+    if dX is not None:
+        _check_matrix("dX", dX, n)
+        _same_shape("dX", dX, dY)
     check(lib().givens_gemm_backward(n, m, _ptr(theta), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY), dY.stride(0),
                                      _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
-                                     FLAG_RECOMPUTE if recompute else 0, *_lay(layout, n, Y.device), _ptr(ws),
+                                     _flags(recompute), *_lay(layout, n, Y.device), _ptr(ws),
                                      ws.numel(), _stream(Y.device)))
     return dtheta, dX
 
@@ -234,7 +281,8 @@ def index_trace(n: int, direction: int = 0, device=None) -> torch.Tensor:
     """Row ids the kernels pair per (block, slot), as (min, max): int32 [R][S][2] (device)."""
     ne = n_eff(n)
     out = torch.full((ne - 1, ne // 2, 2), -1, dtype=torch.int32, device=device or "cuda")
-    check(lib().givens_index_trace(n, int(direction), _ptr(out), _stream(out.device)))
+    with torch.cuda.device(out.device):
+        check(lib().givens_index_trace(n, int(direction), _ptr(out), _stream(out.device)))
     return out
 
 
@@ -282,6 +330,11 @@ class HostPipeline:
         for k in range(K):
             if k + 1 < K: pipe.submit(X[k+1], dY[k+1])
             dth_host = pipe.step()          # forward + backward of the oldest submitted batch
+
+    step() returns a pinned host tensor that holds that batch's dtheta when step() returns (it
+    waits for the device->host copy; the other submitted batch's copy and compute stay queued). Two
+    host buffers alternate, so a result stays valid until the step after next; clone it to keep it.
+    step(wait=False) returns (buffer, event) without waiting: the caller synchronises the event.
     """
 
     def __init__(self, theta, n, m, mask=None, want_dX=False, device=None, allreduce=None):
@@ -295,7 +348,8 @@ class HostPipeline:
         self.Y = torch.empty(n, m, device=dev)
         self.dX = torch.empty(n, m, device=dev) if want_dX else None
         self.dth = torch.empty(num_angles(n), device=dev)
-        self.dth_host = torch.empty(num_angles(n), dtype=torch.float32).pin_memory()
+        self.dth_host = [torch.empty(num_angles(n), dtype=torch.float32).pin_memory() for _ in range(2)]
+        self.d2h_done = [torch.cuda.Event() for _ in range(2)]
         self.ws = workspace(OP_BACKWARD, n, m, dev)
         self.ready = [torch.cuda.Event() for _ in range(2)]
         self.free = [torch.cuda.Event() for _ in range(2)]
@@ -311,7 +365,7 @@ class HostPipeline:
             self.ready[s].record(self.copy)
         self.n_sub += 1
 
-    def step(self):
+    def step(self, wait: bool = True):
         s = self.n_done % 2
         self.compute.wait_event(self.ready[s])
         apply(self.theta, self.X[s], mask=self.mask, out=self.Y, ws=self.ws)
@@ -320,9 +374,14 @@ class HostPipeline:
         self.free[s].record(self.compute)
         if self.allreduce is not None:
             self.allreduce(self.dth)
-        self.dth_host.copy_(self.dth, non_blocking=True)
+        out = self.dth_host[s]
+        out.copy_(self.dth, non_blocking=True)
+        self.d2h_done[s].record(self.compute)
         self.n_done += 1
-        return self.dth_host
+        if not wait:
+            return out, self.d2h_done[s]
+        self.d2h_done[s].synchronize()
+        return out
 
 
 # ---------------------------------------------------------------- unitary U(n) (Appendix A)
@@ -343,6 +402,7 @@ def _check_phi(phi, n):
         raise ValueError(f"phi must be a contiguous CUDA float32 tensor of {N} phase angles")
 
 
+@_on_device
 def u_apply(theta, phi, X, mask=None, adjoint: bool = False, out=None, ws=None, layout: Layout | None = None):
     """Y = U(theta, phi) X or U^dagger X (Algorithm 4), X complex64 [n, m]."""
     n, m = X.shape
@@ -351,6 +411,7 @@ def u_apply(theta, phi, X, mask=None, adjoint: bool = False, out=None, ws=None, 
     _check_phi(phi, n)
     Y = torch.empty_like(X) if out is None else out
     _check_cmatrix("out", Y, n)
+    _same_shape("out", Y, X)
     if ws is None:
         ws = workspace(OP_U_APPLY, n, m, X.device)
     check(lib().givens_u_apply_ex(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y),
@@ -359,6 +420,7 @@ def u_apply(theta, phi, X, mask=None, adjoint: bool = False, out=None, ws=None, 
     return Y
 
 
+@_on_device
 def u_build_U(theta, phi, n: int, mask=None, out=None, ws=None, layout: Layout | None = None):
     """U = U(theta, phi) in U(n), complex64 [n, n]."""
     _check_theta(theta, mask, n)
@@ -372,12 +434,14 @@ def u_build_U(theta, phi, n: int, mask=None, out=None, ws=None, layout: Layout |
     return U
 
 
+@_on_device
 def u_backward(theta, phi, Y, dY, mask=None, want_dX: bool = True, ws=None, recompute: bool = True,
                layout: Layout | None = None):
     """(dtheta, dphi, dX) for a real loss of Y = U X, dY = dL/dRe(Y) + i dL/dIm(Y)."""
     n, m = Y.shape
     _check_cmatrix("Y", Y, n)
     _check_cmatrix("dY", dY, n)
+    _same_shape("dY", dY, Y)
     _check_theta(theta, mask, n)
     _check_phi(phi, n)
     if ws is None:
@@ -389,6 +453,6 @@ def u_backward(theta, phi, Y, dY, mask=None, want_dX: bool = True, ws=None, reco
     dX = torch.empty_like(dY) if want_dX else None
     check(lib().givens_u_backward_ex(n, m, _ptr(theta), _ptr(phi), _ptr(mask), _ptr(Y), Y.stride(0), _ptr(dY),
                                      dY.stride(0), _ptr(dX), dX.stride(0) if dX is not None else 0, _ptr(dtheta),
-                                     _ptr(dphi), FLAG_RECOMPUTE if recompute else 0, *_lay(layout, n, Y.device),
+                                     _ptr(dphi), _flags(recompute), *_lay(layout, n, Y.device),
                                      _ptr(ws), ws.numel(), _stream(Y.device)))
     return dtheta, dphi, dX

@@ -6,7 +6,8 @@ counter-based hash (SplitMix64 finaliser), so any rank, any column shard and the
 CPU oracle can regenerate exactly the same values independently.
 
 Recipe (DESIGN.md "Input recipe"):
-  * theta ~ U(-pi, pi) in fp32           ("unrestricted")
+  * theta ~ U(-pi, pi) in fp32           (SURVEY.md c12; PAPER.md:183-188 "unrestricted");
+    parity tests also use U(-8 pi, 8 pi) and special values (+-2 pi, 1e3, -1e4, ...)
   * X, dY, Gamma ~ N(0, 1) in fp32        (Box-Muller on two hashed uniforms)
   * element (row, col) of an n x m tensor is hashed from its flat row-major index
     row * m_total + col, so a column shard [c0, c1) is reproducible on its own.
@@ -46,10 +47,13 @@ def uniform01(seed: int, tid: int, idx: np.ndarray, stream: int = 0) -> np.ndarr
     return (k >> np.uint64(11)).astype(np.float64) * (1.0 / 9007199254740992.0)
 
 
-def theta(n_angles: int, seed: int = 0) -> np.ndarray:
-    """fp32 angles ~ U(-pi, pi), length n_angles, block-major flat order."""
+def theta(n_angles: int, seed: int = 0, half_range: float = np.pi) -> np.ndarray:
+    """fp32 angles ~ U(-half_range, half_range), length n_angles, block-major flat order.
+
+    The default half_range = pi is the bench recipe; the paper's angles are unrestricted reals
+    (PAPER.md:184), so the parity tests also draw wide ranges (e.g. half_range = 8 pi)."""
     u = uniform01(seed, TID_THETA, np.arange(n_angles, dtype=np.uint64))
-    return ((2.0 * u - 1.0) * np.pi).astype(np.float32)
+    return ((2.0 * u - 1.0) * half_range).astype(np.float32)
 
 
 def normal_matrix(n: int, m_total: int, seed: int, tid: int, col0: int = 0, col1: int | None = None,

@@ -75,9 +75,18 @@ def test_parameter_errors_before_enqueue(g):
     # n < 2
     rc = L.givens_apply(1, 4, None, None, None, 4, None, 4, 0, None, 0, None)
     assert rc == _lib.EINVAL and b"n must be" in L.givens_last_error()
-    # NULL workspace
+    # NULL workspace is allowed (stream-ordered allocation inside the call), but only after the
+    # arguments are validated: NULL data pointers are still refused before anything is allocated
     rc = L.givens_apply(8, 4, None, None, None, 4, None, 4, 0, None, 0, None)
-    assert rc == _lib.EINVAL and b"workspace" in L.givens_last_error()
+    assert rc == _lib.EINVAL and b"non-NULL" in L.givens_last_error()
+    # table reuse needs the forward's workspace
+    rc = L.givens_backward(8, 4, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 4, ctypes.c_void_p(16), 4, None, 0,
+                           ctypes.c_void_p(16), _lib.FLAG_REUSE_TABLES, None, 0, None)
+    assert rc == _lib.EINVAL and b"REUSE" in L.givens_last_error()
+    # table reuse of a workspace no forward filled
+    rc = L.givens_backward(8, 4, ctypes.c_void_p(16), None, ctypes.c_void_p(16), 4, ctypes.c_void_p(16), 4, None, 0,
+                           ctypes.c_void_p(16), _lib.FLAG_REUSE_TABLES, ctypes.c_void_p(1 << 20), 10 ** 9, None)
+    assert rc == _lib.EINVAL and b"no forward" in L.givens_last_error()
     # misaligned workspace / too small
     rc = L.givens_apply(8, 4, None, None, None, 4, None, 4, 0, ctypes.c_void_p(256 + 8), 10 ** 9, None)
     assert rc == _lib.EINVAL and b"aligned" in L.givens_last_error()

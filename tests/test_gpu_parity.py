@@ -9,6 +9,7 @@ import pytest
 import torch
 
 import oracle
+from _parity import rel
 import synth
 
 pytestmark = pytest.mark.gpu
@@ -25,9 +26,6 @@ def g():
     return pkg
 
 
-def rel(a, b):
-    nb = np.linalg.norm(b)
-    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
 def _inputs(n, m, seed=0, mask_keep=None, mask_p=None):
