@@ -15,7 +15,7 @@ per step).
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
 
 With --gpus N > 1 and no WORLD_SIZE in the environment, bench.py launches its own N ranks
-(torch.distributed.run, 127.0.0.1) and exits with their status; under a launcher it checks that
+(one process per GPU, torch.distributed.run's environment, 127.0.0.1) and exits with their status; under a launcher it checks that
 WORLD_SIZE == --gpus.
 
 --impl reference times the fp64 CPU oracle (the only reference this paper has: it released no
@@ -429,16 +429,21 @@ def gemm_path_line(g, torch, theta, X, dY, n, m, ring_ms, tf32_peak, reps=10):
 
 # ------------------------------------------------------------------ our arm
 def self_launch(args):
-    """--gpus N > 1 without a launcher: run N ranks under torch.distributed.run (one node,
-    127.0.0.1, a free port) and return their exit status."""
+    """--gpus N > 1 without a launcher: start N ranks of this script on one node, as
+    torch.distributed.run would (RANK / LOCAL_RANK / WORLD_SIZE / MASTER_ADDR=127.0.0.1 / a free
+    MASTER_PORT in each rank's environment), and return the worst exit status."""
     import socket
     sk = socket.socket()
     sk.bind(("127.0.0.1", 0))
     port = sk.getsockname()[1]
     sk.close()
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
-    return subprocess.call(cmd)
+    procs = []
+    for r in range(args.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(args.gpus),
+                   LOCAL_WORLD_SIZE=str(args.gpus), GROUP_RANK="0", MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env))
+    rcs = [p.wait() for p in procs]
+    return max(rcs, key=abs)
 
 
 def main():
