@@ -418,7 +418,7 @@ def gemm_path_line(g, torch, theta, X, dY, n, m, ring_ms, tf32_peak, reps=10):
     N = n * (n - 1) // 2
     gemm_flops = 3 * (3 * 2.0 * n * n * m)  # Y = U X, dX = U^T dY, M = dY Y^T; three TF32 products each
     return {"workload": f"C3 n={n}, m={m}: same outputs as the headline step (Y, dX, dtheta)",
-            "path": "build_U (ring) + 3xTF32 GEMMs (cuBLAS, K-chunked) + Alg. 3 on Gamma (ring replay, X = I)",
+            "path": "build_U (ring) + 3xTF32 GEMMs (own tcgen05 kernel: TMA, in-kernel hi/lo split, TMEM; K-chunked) + Alg. 3 on Gamma (ring replay, X = I)",
             "fwd_ms": round(tf, 4), "bwd_ms": round(tb, 4), "ms_per_step": round(tf + tb, 4),
             "equivalent_rotations_per_s": N * m / ((tf + tb) * 1e-3),
             "speedup_vs_ring": round(ring_ms / (tf + tb), 3),

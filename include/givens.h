@@ -95,6 +95,11 @@ int givens_schedule(int32_t n, int32_t *pairs_host, int64_t *flat_host);
  */
 int givens_mask_from_dims(int32_t n, const uint8_t *excluded_dims_host, uint8_t *mask_host);
 
+/* Forget what this library remembers about the coefficient tables in ws (the reuse tag, see `ws`
+ * above): call it when a workspace is (re)allocated, so that a caching allocator handing out an
+ * old workspace address can never make GIVENS_FLAG_REUSE_TABLES accept stale tables. Host-only. */
+void givens_workspace_reset(const void *ws);
+
 /* Workspace bytes for op (GIVENS_OP_*) at (n, m) (m = complex columns for the GIVENS_OP_U_*
  * ops). Returns 0 for invalid arguments. */
 size_t givens_workspace_bytes(int op, int32_t n, int64_t m);
@@ -225,9 +230,11 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
  * dY X^T = (dY Y^T) U and dtheta = Algorithm 3 on Gamma (computed by the
  * replay backward with X = I). Same argument meanings, layout options and results as
  * givens_apply_ex / givens_backward_ex (within the fp32 tolerances), but: the workspace is
- * givens_gemm_workspace_bytes(n, m) (it holds U and the hi/lo splits: ~4 n m floats), the GEMMs
- * run in cuBLAS (libcublas.so.12, loaded at first use; GIVENS_EUNSUPPORTED if absent; cuBLAS
- * allocates its own handle/workspace once per thread and device), and nothing may alias.
+ * givens_gemm_workspace_bytes(n, m) (U, M, Gamma, K-chunk partials and two staging buffers), the
+ * GEMMs run on the library's own tcgen05 kernel (TMA operand tiles, the hi/lo split inside the
+ * kernel's pipeline, TMEM accumulators; GIVENS_EUNSUPPORTED if the driver has no tensor-map
+ * encoder), operands whose base or leading dimension the TMA cannot describe (16-byte alignment,
+ * ld a multiple of 4) are staged through the workspace, and nothing may alias.
  * givens_gemm_backward with GIVENS_FLAG_REUSE_TABLES reuses the U a givens_gemm_apply with the same
  * inputs left in ws (checked as above); ws = NULL allocates stream-ordered as above.
  * ------------------------------------------------------------------------------------------ */

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 SRC = os.path.join(CSRC, "givens.cu")
 RING_SRC = os.path.join(CSRC, "ring_inst.cu")
 DEPS = [SRC, RING_SRC, os.path.join(CSRC, "ring.cuh"), os.path.join(CSRC, "common.cuh"),
-        os.path.join(CSRC, "gemm_path.inc"),
+        os.path.join(CSRC, "gemm_path.inc"), os.path.join(CSRC, "tc_gemm.cuh"),
         os.path.join(ROOT, "include", "givens.h")]
 LIB = os.path.join(HERE, "libgivens.so")
 OBJ = os.path.join(HERE, "build_obj")
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(run, jobs))
     objs = [os.path.join(OBJ, "givens.o")] + [os.path.join(OBJ, f"ring_{w}_{l}.o") for w, l in RING_CONFIGS]
     tmp = LIB + f".tmp{os.getpid()}"
-    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"])
+    subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs])
     os.replace(tmp, LIB)
     return LIB
 

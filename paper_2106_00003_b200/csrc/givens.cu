@@ -11,7 +11,6 @@
 //   k_dtheta_reduce            stage 2 of the dtheta reduction (fixed CTA order, no atomics);
 //   k_trace / k_trace_generic  index trace for the bit-exact schedule test.
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 #include <math.h>
 #include <stdarg.h>
 #include <stdint.h>
@@ -950,6 +949,10 @@ const char *givens_version(void) { return GIVENS_VERSION; }
 int64_t givens_num_angles(int32_t n) { return n < 2 ? -1 : (int64_t)n * (n - 1) / 2; }
 
 int givens_supported(int32_t n) { return (n >= 2 && n <= 32768) ? 1 : 0; }
+
+void givens_workspace_reset(const void *ws) {
+    if (ws) untag_tables(ws);
+}
 
 int givens_check_perm(int32_t n, const int32_t *perm_host) {
     if (n < 2 || n > 32768) return fail(GIVENS_EINVAL, "n must be in [2, 32768] (got %d)", n);

@@ -108,7 +108,9 @@ def workspace(op: int, n: int, m: int, device=None) -> torch.Tensor:
         nb = workspace_bytes(op, n, m)
     if nb == 0:
         raise ValueError(f"bad workspace query op={op} n={n} m={m}")
-    return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
+    ws = torch.empty(nb, dtype=torch.uint8, device=device)
+    lib().givens_workspace_reset(ctypes.c_void_p(ws.data_ptr()))  # a reused address carries no stale tables
+    return ws
 
 
 def _ptr(t):
@@ -231,7 +233,9 @@ def gemm_workspace(n: int, m: int, device=None) -> torch.Tensor:
         nb = int(lib().givens_gemm_workspace_bytes(n, m))
     if nb == 0:
         raise ValueError(f"bad GEMM workspace query n={n} m={m}")
-    return torch.empty(nb, dtype=torch.uint8, device=device or "cuda")
+    ws = torch.empty(nb, dtype=torch.uint8, device=device)
+    lib().givens_workspace_reset(ctypes.c_void_p(ws.data_ptr()))  # the ring tables sit at offset 0
+    return ws
 
 
 @_on_device
