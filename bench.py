@@ -424,6 +424,9 @@ def gemm_path_line(g, torch, theta, X, dY, n, m, ring_ms, tf32_peak, reps=10):
             "speedup_vs_ring": round(ring_ms / (tf + tb), 3),
             "tf32_gemm_flops_per_step": gemm_flops,
             "tf32_peak_tflops": tf32_peak,
+            # the whole step's TF32 tensor-core work over the whole step's time (U-build and Alg. 3 included)
+            "tf32_achieved_tflops_step": gemm_flops / ((tf + tb) * 1e-3) / 1e12,
+            "tf32_frac_step": gemm_flops / ((tf + tb) * 1e-3) / 1e12 / tf32_peak,
             "note": "not the headline: the headline is the SURVEY 8(a) ring path; this is the 8(f2) row"}
 
 

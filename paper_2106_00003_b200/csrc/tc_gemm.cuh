@@ -7,10 +7,12 @@
 //   warp 1      MMA issuer (one elected thread): per 32-wide k-block 3 x 4 tcgen05.mma.kind::tf32
 //               (M = 128, N = BN, K = 8) into a TMEM accumulator; tcgen05.commit frees the stage;
 //   warp 2      TMEM allocator;
-//   warps 4-7   the 3xTF32 split in the pipeline: per stage they turn the raw tile into hi (round
-//               to nearest TF32, in place) and lo = x - hi (a second buffer of the same swizzled
-//               layout -- the split is elementwise, so it never needs to know the swizzle), then
-//               fence the async proxy and arrive; after the mainloop they are the epilogue:
+//   warps 4-7   the 3xTF32 split in the pipeline: the tensor core reads an fp32 operand as TF32 by
+//               truncation (the low 13 mantissa bits ignored; measured by tools/tc_trunc.cu), so the
+//               raw tile already is "hi" = trunc(x); per stage they write lo = x - trunc(x) (exact in
+//               fp32) into a second buffer of the same swizzled layout -- the split is elementwise,
+//               so it never needs to know the swizzle -- then fence the async proxy and arrive;
+//               after the mainloop they are the epilogue:
 //               tcgen05.ld of the accumulator, stored to global with the M index contiguous.
 // Operand layouts (both operands are described as "rows x K" = M x K for A and N x K for B):
 //   K-major  : element (r, k) at p + r ld + k  -- TMA box {32 k, R rows}, canonical K-major SW128
@@ -31,9 +33,9 @@
 
 namespace tcg {
 
-constexpr int BM = 128, BN = 128, BK = 32, NST = 3;
+constexpr int BM = 128, BN = 256, BK = 32, NST = 2;
 constexpr int TILE_A = BM * BK * 4;            // 16 KB
-constexpr int TILE_B = BN * BK * 4;            // 16 KB
+constexpr int TILE_B = BN * BK * 4;            // 32 KB
 constexpr int HI_BYTES = TILE_A + TILE_B;      // raw / hi part of a stage
 constexpr int STAGE_BYTES = 2 * HI_BYTES;      // hi A | hi B | lo A | lo B
 constexpr int NTHREADS = 256;
@@ -47,6 +49,15 @@ struct Args {
     int accumulate;       // 1: out += D (K cut into sequential launches), 0: out = D
 };
 
+// the same box delivered to the same shared-memory offset (and barrier) of every CTA in ctamask
+__device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar,
+                                               uint16_t ctamask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(gk::smem_u32(dst)), "l"(map), "r"(c0), "r"(c1), "r"(gk::smem_u32(bar)), "h"(ctamask)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
@@ -82,6 +93,20 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
         ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
+// arrive on the barrier at this offset in every CTA of ctamask once this thread's MMAs are done
+__device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t ctamask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(gk::smem_u32(bar)), "h"(ctamask)
+                 : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(gk::smem_u32(bar))
                  : "memory");
@@ -89,11 +114,16 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-// round-to-nearest TF32 (10-bit mantissa; exact in fp32) and the exact fp32 remainder
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u); }
+// x - trunc_tf32(x): exact in fp32 (the low 13 mantissa bits of x)
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+
+// Clusters of CL = 2 CTAs along M share their B tile: each loads half of it with a multicast TMA
+// into both CTAs' stage (B's L2 -> SM traffic halves), and each CTA's MMA commit releases the stage in
+// both (empty barriers count CL arrivals), so neither overwrites a stage its peer still reads.
+constexpr int CL = 2;
 
 template <bool AMN, bool BMN>
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __cluster_dims__(1, CL, 1) __launch_bounds__(NTHREADS, 1)
 k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Args a) {
     extern __shared__ uint8_t smem_raw[];
     // SWIZZLE_128B atoms need 1024-byte alignment
@@ -105,7 +135,9 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accb + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    // n-tiles vary fastest: the CTAs that share an A tile (the streamed operand) run at the same time,
+    // so it comes from DRAM once and from L2 for the others
+    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
     const int kbeg = blockIdx.z * a.kchunk;
     const int kend = min(a.K, kbeg + a.kchunk);
     const int nkb = (kend - kbeg + BK - 1) / BK;
@@ -114,7 +146,7 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
         for (int s = 0; s < NST; s++) {
             gk::mbar_init(&full[s], 1);
             gk::mbar_init(&conv[s], 4);
-            gk::mbar_init(&empty[s], 1);
+            gk::mbar_init(&empty[s], CL);
         }
         gk::mbar_init(accb, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -127,8 +159,11 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // both CTAs' barriers exist before any multicast write or remote arrive
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t crank = cluster_rank();
+    constexpr uint16_t kMask = (1u << CL) - 1;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -146,12 +181,16 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
                 } else {
                     tma_load_2d(st, &tma_a, k0, m0, &full[s]);
                 }
+                // this CTA's half of B, multicast into both CTAs of the cluster
                 if constexpr (BMN) {
 #pragma unroll
-                    for (int b = 0; b < BN / 32; b++)
-                        tma_load_2d(st + TILE_A + b * 4096, &tma_b, n0 + 32 * b, k0, &full[s]);
+                    for (int b = 0; b < BN / 32 / CL; b++) {
+                        const int bb = (int)crank * (BN / 32 / CL) + b;
+                        tma_load_2d_mc(st + TILE_A + bb * 4096, &tma_b, n0 + 32 * bb, k0, &full[s], kMask);
+                    }
                 } else {
-                    tma_load_2d(st + TILE_A, &tma_b, k0, n0, &full[s]);
+                    tma_load_2d_mc(st + TILE_A + crank * (TILE_B / CL), &tma_b, k0, n0 + (int)crank * (BN / CL),
+                                   &full[s], kMask);
                 }
             }
         }
@@ -171,11 +210,16 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
                     const uint64_t dbh = odesc<BMN>(bhi, ks), dbl = odesc<BMN>(blo, ks);
                     const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
                     // small cross terms first, then hi x hi
+#ifndef TCG_ONE_MMA
                     mma_tf32(tmem, dah, dbl, idesc, acc0);
                     mma_tf32(tmem, dal, dbh, idesc, 1u);
                     mma_tf32(tmem, dah, dbh, idesc, 1u);
+#else
+                    (void)dal; (void)dbl;
+                    mma_tf32(tmem, dah, dbh, idesc, acc0);
+#endif
                 }
-                mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+                mma_commit_mc(&empty[s], kMask);  // frees the stage (in both CTAs) once these MMAs have read it
             }
             mma_commit(accb);  // the accumulator is complete
         }
@@ -187,13 +231,15 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
             gk::mbar_wait(&full[s], (uint32_t)(j & 1));
             float4 *hi = reinterpret_cast<float4 *>(smem + (size_t)s * STAGE_BYTES);
             float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)s * STAGE_BYTES + HI_BYTES);
+#ifndef TCG_NO_CONVERT
 #pragma unroll 4
             for (int i = t; i < HI_BYTES / 16; i += 128) {
                 const float4 x = hi[i];
-                const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-                hi[i] = h;
-                lo[i] = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+                lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
             }
+#else
+            (void)hi; (void)lo;
+#endif
             gk::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
 #ifdef TCG_DEBUG
             if (t == 0 && kb == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
@@ -244,6 +290,7 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync_all();  // no CTA leaves while its peer may still write its smem or arrive on its barriers
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN));
@@ -307,7 +354,7 @@ template <bool AMN, bool BMN>
 inline cudaError_t gemm3_launch(const Operand &A, const Operand &B, int M, int N, int K, int kchunk, float *out,
                                 int64_t ldo, int64_t zstride, int accumulate, cudaStream_t st) {
     CUtensorMap ma, mb;
-    if (!make_map(&ma, A.p, M, K, A.ld, AMN, BM) || !make_map(&mb, B.p, N, K, B.ld, BMN, BN))
+    if (!make_map(&ma, A.p, M, K, A.ld, AMN, BM) || !make_map(&mb, B.p, N, K, B.ld, BMN, BN / CL))
         return cudaErrorNotSupported;
     static bool attr = [] {
         return cudaFuncSetAttribute(k_gemm3<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) ==
@@ -315,7 +362,8 @@ inline cudaError_t gemm3_launch(const Operand &A, const Operand &B, int M, int N
     }();
     if (!attr) return cudaErrorInvalidConfiguration;
     Args a{M, N, K, kchunk, out, ldo, zstride, accumulate};
-    dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN), (unsigned)((K + kchunk - 1) / kchunk));
+    const int mt = (M + BM - 1) / BM;  // M tiles, padded to whole clusters (a padding CTA loads zeros, stores nothing)
+    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((mt + CL - 1) / CL * CL), (unsigned)((K + kchunk - 1) / kchunk));
     k_gemm3<AMN, BMN><<<grid, NTHREADS, SMEM_BYTES, st>>>(ma, mb, a);
     return cudaGetLastError();
 }
