@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libgivens.so")
 OBJ = os.path.join(HERE, "build_obj")
 # (W, L) ring configurations; must match GK_RING_CONFIGS in csrc/givens.cu
 RING_CONFIGS = [(4, 1), (8, 1), (16, 1), (32, 1), (16, 4), (16, 8), (16, 16), (16, 32), (8, 64), (16, 64),
-                (32, 32), (16, 128), (8, 32), (8, 128)]
+                (32, 32), (16, 128), (8, 32), (8, 128), (8, 16)]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

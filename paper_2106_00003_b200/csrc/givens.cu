@@ -34,6 +34,7 @@ namespace gk {
 #define GK_DECL(W, L) cudaError_t ring_launch_##W##_##L(int mode, const RingArgs &ra, int64_t grid, cudaStream_t st);
 GK_DECL(4, 1) GK_DECL(8, 1) GK_DECL(16, 1) GK_DECL(32, 1) GK_DECL(16, 4) GK_DECL(16, 8) GK_DECL(16, 16)
 GK_DECL(16, 32) GK_DECL(8, 64) GK_DECL(16, 64) GK_DECL(32, 32) GK_DECL(16, 128) GK_DECL(8, 32) GK_DECL(8, 128)
+GK_DECL(8, 16)
 #undef GK_DECL
 }  // namespace gk
 
@@ -69,7 +70,17 @@ struct Cfg {
 
 bool is_pow2(int x) { return x > 0 && (x & (x - 1)) == 0; }
 
-Cfg make_cfg(int n) {
+int dev_sms();
+int64_t cols_per_slab(const Cfg &c, int mode);
+
+// m: the batch the configuration will serve (real columns; -1 = unknown). The real ring at S = 128 /
+// 256 (n = 256 / 512) switches from W = 16 to W = 8 slots per lane (twice the lanes per column, so
+// twice the slabs) when the narrow W = 16 launch would leave more than half the SMs without a slab
+// -- the U-build and its gradient at those n (measured: n = 256 gradient 104 -> 72 us, n = 512
+// 201 -> 140 us), not C2 (128 slabs already; W = 8 would need two waves). Forward and backward of
+// one batch see the same m, hence the same configuration (the reuse tag checks it).
+Cfg make_cfg(int n, int64_t m = -1);
+Cfg make_cfg(int n, int64_t m) {
     Cfg c;
     c.ne = n + (n & 1);
     c.S = c.ne / 2;
@@ -87,7 +98,7 @@ Cfg make_cfg(int n) {
         c.fast = 1; c.W = c.S; c.L = 1;
     } else if (is_pow2(c.S) && c.S >= 64 && c.S <= 512) {
         c.fast = 1; c.W = 16; c.L = c.S / 16;
-        if (c.S == 512 && wpref == 8) { c.W = 8; c.L = 64; }
+        if (wpref == 8 && c.S >= 128) { c.W = 8; c.L = c.S / 8; }
     } else if (c.S == 1024) {
         c.fast = 1; c.W = 16; c.L = 64;
         if (wpref == 32) { c.W = 32; c.L = 32; }
@@ -107,6 +118,12 @@ Cfg make_cfg(int n) {
         }
     }
     c.rowbytes = ((c.S * 8) + 15) / 16 * 16;  // == S*8 for every ring configuration
+    if (m > 0 && wpref == 0 && c.fast && c.W == 16 && (c.S == 128 || c.S == 256)) {
+        Cfg w8 = c;
+        w8.W = 8; w8.L = w8.La = c.S / 8;
+        const int64_t narrow16 = (m + cols_per_slab(c, M_FWD | M_NARROW) - 1) / cols_per_slab(c, M_FWD | M_NARROW);
+        if (2 * narrow16 <= dev_sms()) return w8;
+    }
     return c;
 }
 
@@ -129,7 +146,7 @@ Cfg make_cfg_u(int n) {
     return c;
 }
 
-Cfg cfg_for_op(int n, int op) { return op >= 3 ? make_cfg_u(n) : make_cfg(n); }
+Cfg cfg_for_op(int n, int op, int64_t m) { return op >= 3 ? make_cfg_u(n) : make_cfg(n, m); }
 
 int dev_sms() {
     static std::mutex mu;
@@ -237,7 +254,7 @@ struct AutoWs {
 };
 
 struct WsLayout {
-    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, segx, lay, partial, scratch, total;
+    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, lay, partial, scratch, total;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
@@ -259,7 +276,6 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     L.flip = off; off = al256(off + (size_t)c.R * c.S);
     L.sig = off; off = al256(off + (size_t)c.R * c.ne);
     L.sfin = off; off = al256(off + (size_t)c.ne);
-    L.segx = off; off = al256(off + (size_t)32 * c.ne);
     L.lay = off; off = al256(off + (size_t)(c.ne + 2) * 4);
     L.partial = off;
     if (base == GIVENS_OP_BACKWARD) {
@@ -302,6 +318,15 @@ __global__ void k_layout(int n, int ne, const int32_t *__restrict__ perm, int re
     }
 }
 
+// The precompute kernels read the layout block only under a start permutation; without one (lay ==
+// NULL) label l is row l, the odd-n bye is label n_eff - 1 and the reflected column's label is the
+// column itself -- and k_layout is not launched at all.
+__device__ __forceinline__ int lay_row(const int32_t *__restrict__ lay, int l) { return lay ? lay[l] : l; }
+__device__ __forceinline__ int lay_bye(const int32_t *__restrict__ lay, int ne) { return lay ? lay[ne] : ne - 1; }
+__device__ __forceinline__ int lay_refl(const int32_t *__restrict__ lay, int ne, int refl) {
+    return lay ? lay[ne + 1] : refl;
+}
+
 // theta -> the angle phi in [-pi/2, pi/2] with R(theta) = (-1)^flip R(phi). theta is
 // any real (theta in R^N): it is first reduced to [-pi, pi] by the exact fp64
 // remainder modulo 2 pi (R is 2 pi-periodic), then flipped by pi when |.| > pi/2, so the shear
@@ -322,7 +347,7 @@ __global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uin
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)R * S) return;
     int r = (int)(idx / S), k = (int)(idx % S);
-    int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
+    int64_t f = flat_of_bl(r, k, n, ne, lay_bye(lay, ne));
     uint8_t fl = 0;
     if (f >= 0 && (!mask || mask[f])) {
         int fb;
@@ -346,24 +371,24 @@ __device__ __forceinline__ uint32_t flip_of(const uint8_t *__restrict__ flip, in
     return (uint32_t)flip[(int64_t)r * (ne / 2) + k];
 }
 
-__global__ void k_sigma_seg(int ne, const uint8_t *__restrict__ flip, uint8_t *__restrict__ segx) {
-    const int R = ne - 1, i = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
-    if (i >= ne) return;
+// One kernel: a CTA of 32 rows x 32 segments; thread (row i, segment c) XORs its segment's flips into
+// shared memory, then starts from the XOR of the segments before it and writes sig (and sfin).
+__global__ void __launch_bounds__(1024) k_sigma(int ne, const uint8_t *__restrict__ flip,
+                                                const int32_t *__restrict__ lay, int refl,
+                                                uint8_t *__restrict__ sig, uint8_t *__restrict__ sfin) {
+    __shared__ uint8_t segx[32][33];
+    const int R = ne - 1, tx = threadIdx.x, c = threadIdx.y, i = blockIdx.x * 32 + tx;
     const int seg = (R + 31) / 32, hi = R - 1 - c * seg, lo = max(hi - seg + 1, 0);
     uint32_t x = 0;
-    for (int r = hi; r >= lo; r--) x ^= flip_of(flip, i, r, ne);
-    segx[(int64_t)c * ne + i] = (uint8_t)x;
-}
-
-__global__ void k_sigma_fill(int ne, const uint8_t *__restrict__ flip, const uint8_t *__restrict__ segx,
-                             const int32_t *__restrict__ lay, uint8_t *__restrict__ sig, uint8_t *__restrict__ sfin) {
-    const int R = ne - 1, i = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+    if (i < ne)
+        for (int r = hi; r >= lo; r--) x ^= flip_of(flip, i, r, ne);
+    segx[c][tx] = (uint8_t)x;
+    __syncthreads();
     if (i >= ne) return;
-    const int seg = (R + 31) / 32, hi = R - 1 - c * seg, lo = max(hi - seg + 1, 0);
     uint32_t par = 0;
-    for (int cc = 0; cc < c; cc++) par ^= segx[(int64_t)cc * ne + i];
-    const uint32_t rf = (lay[ne + 1] == i) ? 1u : 0u;
-    if (c == 31) sfin[i] = (uint8_t)(par ^ segx[(int64_t)31 * ne + i] ^ rf);
+    for (int cc = 0; cc < c; cc++) par ^= segx[cc][tx];
+    const uint32_t rf = (lay_refl(lay, ne, refl) == i) ? 1u : 0u;
+    if (c == 31) sfin[i] = (uint8_t)(par ^ segx[31][tx] ^ rf);
     par ^= rf;
     for (int r = hi; r >= lo; r--) {
         sig[(int64_t)r * ne + i] = (uint8_t)par;
@@ -398,11 +423,11 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
     }
     int r = rho - 1;
     int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);  // labels; rows lay[a], lay[b]
-    int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
+    int64_t f = flat_of_bl(r, k, n, ne, lay_bye(lay, ne));
     bool active = f >= 0 && (!mask || mask[f]);
     double th = active ? (double)theta[f] : 0.0;
     const double phi = reduce_angle(th, nullptr);
-    int neg = (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) ^ (lay[a] > lay[b] ? 1 : 0);
+    int neg = (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) ^ (lay_row(lay, a) > lay_row(lay, b) ? 1 : 0);
     double tq = tan(0.5 * phi), sq = sin(phi);
     if (neg) { tq = -tq; sq = -sq; }
     row[pos] = make_float2((float)tq, (float)sq);
@@ -438,12 +463,12 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
     }
     int r = rho - 1;
     int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);
-    int64_t f = flat_of_bl(r, k, n, ne, lay[ne]);
+    int64_t f = flat_of_bl(r, k, n, ne, lay_bye(lay, ne));
     bool active = f >= 0 && (!mask || mask[f]);
     double th = active ? (double)theta[f] : 0.0, pv = active ? (double)phi[f] : 0.0;
     const double thr = reduce_angle(th, nullptr);
     float pc = (float)cos(pv), ps = (float)sin(pv);
-    bool top_is_i = lay[a] < lay[b];
+    bool top_is_i = lay_row(lay, a) < lay_row(lay, b);
     phr[pos_ph] = top_is_i ? make_float4(pc, ps, 1.f, 0.f) : make_float4(1.f, 0.f, pc, ps);
     {   // FFMA2-ready pairs per side, top then bottom: (p, q, -q, p) forward, (p, -q, q, p) adjoint
         const int64_t pp0 = (int64_t)rho * 2 * S + (2 * q) * L + t, pp1 = pp0 + L;
@@ -460,24 +485,30 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
 }
 
 // ------------------------------------------------------------------ stage-2 dtheta reduction
-// dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in fixed CTA order (PAPER.md:768-781
-// "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0.
-__global__ void k_dtheta_reduce(int S, int W, int L, int NW, int G, int ring, int vals, const float *__restrict__ partial,
-                                const int32_t *__restrict__ amap, float *__restrict__ dtheta, float *__restrict__ dphi) {
-    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    int rows = 2 * S;
-    if (idx >= (int64_t)rows * S) return;
-    int32_t code = amap[idx];
-    if (code < 0) return;
-    int64_t f = code & 0x1FFFFFFF;
-    if (code & (1 << 29)) {
+// dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in a fixed order (PAPER.md:768-781
+// "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0. A CTA handles 32
+// consecutive table slots x 8 CTA phases: thread (x, y) sums the CTAs y, y + 8, y + 16, ... in
+// increasing order (eight independent load chains instead of one G-long one, each warp reading 32
+// consecutive floats), then row y = 0 adds the eight phase sums in order 0..7.
+constexpr int kRedPh = 8;
+__global__ void __launch_bounds__(32 * kRedPh) k_dtheta_reduce(int S, int W, int L, int NW, int G, int ring, int vals,
+                                                               const float *__restrict__ partial,
+                                                               const int32_t *__restrict__ amap,
+                                                               float *__restrict__ dtheta, float *__restrict__ dphi) {
+    __shared__ float ph[kRedPh][32];
+    const int64_t idx = (int64_t)blockIdx.x * 32 + threadIdx.x;
+    const int rows = 2 * S, y = threadIdx.y;
+    const bool in = idx < (int64_t)rows * S;
+    const int32_t code = in ? amap[idx] : -1;
+    const int64_t f = code & 0x1FFFFFFF;
+    const bool live = code >= 0 && !(code & (1 << 29));
+    if (code >= 0 && (code & (1 << 29)) && y == 0) {
         dtheta[f] = 0.f;
         if (vals > 1) dphi[f] = 0.f;
-        return;
     }
-    int rho = (int)(idx / S), k = (int)(idx % S);
+    const int rho = in ? (int)(idx / S) : 0, k = in ? (int)(idx % S) : 0;
     for (int v = 0; v < vals; v++) {
-        int64_t pos, stride;
+        int64_t pos = 0, stride = 0;
         if (ring) {
             // ring kernel layout: per CTA, per group of RG steps, NW warp blocks of RG x OUTCH float4;
             // slot k (lane t = k / W of the group, slot q = k % W) is chunk ci = v*NCHW1 + (q/4)*LW + t%LW
@@ -497,11 +528,21 @@ __global__ void k_dtheta_reduce(int S, int W, int L, int NW, int G, int ring, in
             pos = ((int64_t)v * rows + rho) * S + k;  // generic kernel: natural order, [vals][rows][S]
             stride = (int64_t)vals * rows * S;
         }
-        float s = 0.f;
-        const float *p = partial + pos;
-        for (int cc = 0; cc < G; cc++) s += p[(int64_t)cc * stride];
-        if (v == 0) dtheta[f] = (code & (1 << 30)) ? -s : s;
-        else dphi[f] = s;  // dphi carries no sign: sigma_i^2 = 1
+        float sp = 0.f;
+        if (live) {
+            const float *p = partial + pos;
+            for (int cc = y; cc < G; cc += kRedPh) sp += p[(int64_t)cc * stride];
+        }
+        ph[y][threadIdx.x] = sp;
+        __syncthreads();
+        if (y == 0 && live) {
+            float s2 = ph[0][threadIdx.x];
+#pragma unroll
+            for (int jj = 1; jj < kRedPh; jj++) s2 += ph[jj][threadIdx.x];
+            if (v == 0) dtheta[f] = (code & (1 << 30)) ? -s2 : s2;
+            else dphi[f] = s2;  // dphi carries no sign: sigma_i^2 = 1
+        }
+        __syncthreads();
     }
 }
 
@@ -797,7 +838,7 @@ using namespace gk;
 
 // ring configurations compiled in ring_inst.cu (one object per (W, L))
 #define GK_RING_CONFIGS(X) X(4, 1) X(8, 1) X(16, 1) X(32, 1) X(16, 4) X(16, 8) X(16, 16) X(16, 32) X(8, 64) \
-    X(16, 64) X(32, 32) X(16, 128) X(8, 32) X(8, 128)
+    X(16, 64) X(32, 32) X(16, 128) X(8, 32) X(8, 128) X(8, 16)
 
 int launch_ring(int mode, const Cfg &c, RingArgs &ra, int64_t grid, cudaStream_t st) {
     cudaError_t e = cudaErrorInvalidConfiguration;
@@ -825,18 +866,18 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
                    cudaStream_t st, const float *phi = nullptr, Lay lo = kNoLay) {
     int64_t RS = (int64_t)c.R * c.S;
     untag_tables(ws);  // partially rebuilt tables must not pass for the old ones if a launch fails
-    int32_t *lay = reinterpret_cast<int32_t *>(ws + L.lay);
-    k_layout<<<1, 1024, 0, st>>>(n, c.ne, lo.perm, lo.refl, lay);
-    CUDA_TRY(cudaGetLastError());
-    k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, lay, ws + L.flip);
-    CUDA_TRY(cudaGetLastError());
-    {
-        const dim3 grid((unsigned)((c.ne + 127) / 128), 32);
-        k_sigma_seg<<<grid, 128, 0, st>>>(c.ne, ws + L.flip, ws + L.segx);
-        CUDA_TRY(cudaGetLastError());
-        k_sigma_fill<<<grid, 128, 0, st>>>(c.ne, ws + L.flip, ws + L.segx, lay, ws + L.sig, ws + L.sfin);
+    // the layout block only under a start permutation (the kernels take lay == NULL as the identity)
+    int32_t *lay = nullptr;
+    if (lo.perm) {
+        lay = reinterpret_cast<int32_t *>(ws + L.lay);
+        k_layout<<<1, 1024, 0, st>>>(n, c.ne, lo.perm, lo.refl, lay);
         CUDA_TRY(cudaGetLastError());
     }
+    k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, lay, ws + L.flip);
+    CUDA_TRY(cudaGetLastError());
+    k_sigma<<<(unsigned)((c.ne + 31) / 32), dim3(32, 32), 0, st>>>(c.ne, ws + L.flip, lay, lo.refl, ws + L.sig,
+                                                                     ws + L.sfin);
+    CUDA_TRY(cudaGetLastError());
     int64_t tot = (int64_t)(c.R + 2) * c.S;
     int W = c.fast ? c.W : c.S, Lq = c.fast ? c.La : 1;
     k_coef<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, c.rowbytes, theta, mask, ws + L.flip,
@@ -1014,7 +1055,7 @@ int givens_mask_from_dims(int32_t n, const uint8_t *excl, uint8_t *mask) {
 
 size_t givens_workspace_bytes(int op, int32_t n, int64_t m) {
     if (n < 2 || n > 32768 || m < 0 || op < 0 || op > 5) return 0;
-    Cfg c = cfg_for_op(n, op);
+    Cfg c = cfg_for_op(n, op, (op % 3) == GIVENS_OP_BUILD_U ? n : m);
     return ws_layout(c, op, (op % 3) == GIVENS_OP_BUILD_U ? n : m).total;
 }
 
@@ -1088,7 +1129,7 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
     if ((rc = run_apply_mode(M_BWD | M_UNI, n, 2 * m, Y, 2 * ldy, dY, 2 * lddy, dX, 2 * lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD | M_UNI, 2 * m);
     int64_t tot = (int64_t)2 * c.S * c.S;
-    k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+    k_dtheta_reduce<<<(unsigned)((tot + 31) / 32), dim3(32, kRedPh), 0, st>>>(
         c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD | M_UNI, 2 * m)), (int)G, c.fast, 2,
         reinterpret_cast<const float *>(w + L.partial),
         reinterpret_cast<const int32_t *>(w + L.amap), dtheta, dphi);
@@ -1104,7 +1145,7 @@ int givens_apply_ex(int32_t n, int64_t m, const float *theta, const uint8_t *mas
     if (!theta || (m > 0 && (!X || !Y))) return fail(GIVENS_EINVAL, "theta, X and Y must be non-NULL");
     if (ldx < m || ldy < m) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (X == Y && ldx != ldy) return fail(GIVENS_EINVAL, "in-place apply needs ldx == ldy");
-    Cfg c = make_cfg(n);
+    Cfg c = make_cfg(n, m);
     WsLayout L = ws_layout(c, GIVENS_OP_APPLY, m);
     cudaStream_t st = (cudaStream_t)stream;
     AutoWs aw;
@@ -1122,7 +1163,7 @@ int givens_build_U_ex(int32_t n, const float *theta, const uint8_t *mask, float 
     if (reflect_col < -1 || reflect_col >= n) return fail(GIVENS_EINVAL, "reflect_col must be -1 or in [0, n)");
     if (!theta || !U) return fail(GIVENS_EINVAL, "theta and U must be non-NULL");
     if (ldu < n) return fail(GIVENS_EINVAL, "ldu < n");
-    Cfg c = make_cfg(n);
+    Cfg c = make_cfg(n, n);
     WsLayout L = ws_layout(c, GIVENS_OP_BUILD_U, n);
     cudaStream_t st = (cudaStream_t)stream;
     AutoWs aw;
@@ -1141,7 +1182,7 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
     if (!theta || !dtheta || (m > 0 && (!Y || !dY))) return fail(GIVENS_EINVAL, "theta, Y, dY and dtheta must be non-NULL");
     if (ldy < m || lddy < m || (dX && lddx < m)) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
     if (dX && dX == dY && lddx != lddy) return fail(GIVENS_EINVAL, "in-place dX needs lddx == lddy");
-    Cfg c = make_cfg(n);
+    Cfg c = make_cfg(n, m);
     WsLayout L = ws_layout(c, GIVENS_OP_BACKWARD, m);
     cudaStream_t st = (cudaStream_t)stream;
     if (flags & GIVENS_FLAG_REUSE_TABLES) {
@@ -1161,7 +1202,7 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
     if ((rc = run_apply_mode(M_BWD, n, m, Y, ldy, dY, lddy, dX, lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD, m);
     int64_t tot = (int64_t)2 * c.S * c.S;
-    k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+    k_dtheta_reduce<<<(unsigned)((tot + 31) / 32), dim3(32, kRedPh), 0, st>>>(
         c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD, m)), (int)G, c.fast, 1,
         reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
         dtheta, nullptr);

@@ -53,7 +53,7 @@ static double check(bool amn, bool bmn, int M, int N, int K, int kchunk) {
     return sqrt(num / den);
 }
 
-static void timeit(const char *name, bool amn, bool bmn, int M, int N, int K, int kchunk) {
+static double timeit(const char *name, bool amn, bool bmn, int M, int N, int K, int kchunk) {
     int64_t lda = amn ? M : K, ldb = bmn ? N : K;
     size_t na = (size_t)lda * (amn ? K : M), nb = (size_t)ldb * (bmn ? K : N);
     float *da, *db, *dd;
@@ -76,9 +76,10 @@ static void timeit(const char *name, bool amn, bool bmn, int M, int N, int K, in
     printf("%-34s M=%6d N=%5d K=%6d: %.3f ms  %.1f TF/s (3xTF32: %.1f TF/s of TF32 MMA)  %s\n", name, M, N, K, ms,
            fl / 3 / ms / 1e9, fl / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
     cudaFree(da); cudaFree(db); cudaFree(dd);
+    return ms;
 }
 
-int main() {
+int main(int argc, char **argv) {
     double worst = 0;
     for (int amn = 0; amn < 2; amn++)
         for (int bmn = 0; bmn < 2; bmn++) {
@@ -91,5 +92,21 @@ int main() {
     timeit("dX^T = dY^T U   (A MN, B MN)", true, true, 65536, 1024, 1024, 1 << 20);
     timeit("M^T = Y dY^T    (A K, B K, split)", false, false, 1024, 1024, 65536, 2048);
     timeit("Gam^T = U^T M^T (A MN, B K)", true, false, 1024, 1024, 1024, 1 << 20);
+    // The north_star's k-round dense-tile family at C3 (n = 1024, m = 65536): k consecutive blocks of
+    // the circle method compose into a matrix that is banded in slot coordinates (every round moves a
+    // value at most one slot, so a 128-row output tile depends on a window of w = 128 + 2 (2k + 2) input
+    // rows). The forward is then ceil(1023 / k) GEMMs of the shape Y^T (m x n) over K = w each (the
+    // k = 1023 member is the dense U: one GEMM over K = n). Time the GEMM at each window; the build of
+    // the band matrices (k rounds of the ring on identity columns, ~ one U-build) comes on top.
+    printf("k-round banded-tile forward (C3), 3xTF32 GEMMs over the band window:\n");
+    for (int k : {16, 32, 64, 128, 256, 1023}) {
+        int w = k >= 1023 ? 1024 : 128 + 2 * (2 * k + 2);
+        if (w > 1024) w = 1024;
+        const int groups = (1023 + k - 1) / k;
+        char nm[64];
+        snprintf(nm, sizeof nm, "band k=%d (window %d)", k, w);
+        double ms = timeit(nm, true, false, 65536, 1024, w, 1 << 20);
+        printf("  k=%4d: %2d GEMMs x %.3f ms = %.3f ms forward (+ band build)\n", k, groups, ms, groups * ms);
+    }
     return 0;
 }
