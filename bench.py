@@ -41,6 +41,7 @@ M_TOTAL = 65536
 SEED = 0
 FP32_LANES_PER_SM = 128           # B200 SM: 4 SMSP x 32 FP32 lanes (B200_PROFILING.md / guide)
 FLOPS_FWD, FLOPS_BWD = 6, 16      # algorithmic flops per rotation-column
+FP32_MICROBENCH_TFLOPS = 71.7     # FFMA loop, 148 SMs at 1965 MHz (profiles/r2b_fp32_microbench.txt)
 SPIN_CYCLES = 4_000_000            # ~2 ms GPU spin ahead of short timed sequences (host enqueue hidden)
 
 
@@ -607,12 +608,17 @@ def main():
                          "peak_basis": f"{n_sm} SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {peak_clock:.0f} MHz "
                                        "(max boost; DESIGN.md §5)",
                          "flops_per_rotation_column": FLOPS_BWD, "ms_per_launch": ms_bwd,
+                         # the FFMA-loop microbenchmark's rate on this pool's B200s (tools/microbench.cu,
+                         # profiles/r2b_fp32_microbench.txt, 1965 MHz): the frac against it, for context
+                         "peak_measured_microbench": FP32_MICROBENCH_TFLOPS,
+                         "frac_vs_microbench": achieved / FP32_MICROBENCH_TFLOPS,
                          # the whole step (precompute + forward + backward) against the same peak, at
                          # 6 + 16 algorithmic flops per rotation-column
                          "step_achieved": (FLOPS_FWD + FLOPS_BWD) * N * m / (ms_step * 1e-3) / 1e12,
                          "step_frac": (FLOPS_FWD + FLOPS_BWD) * N * m / (ms_step * 1e-3) / 1e12 / peak},
             "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd, "step_ms_stats_rank0": step_stats,
-            "gpu_launches": 8 * args.steps,
+            # our kernels per step: k_flip, k_sigma, k_coef (precompute), forward, backward, stage-2 reduce
+            "gpu_launches": 6 * args.steps,
             "clocks": clk,
         }
         if e2e:

@@ -72,7 +72,11 @@ constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose 
 // it La == L is a compile-time constant (fewer registers and address computations)
 // M_NARROW (launch-time only): 4-warp CTAs with at most 2 columns per thread, for batches too
 // small to give every SM a slab at the normal width (U-build and Alg. 3 at n <= 2048, C2)
-enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16 };
+// M_NK4 (launch-time only, with M_NARROW, W = 8 rings): 4 columns per thread instead of 2 -- the same
+// slab width as the W = 16 narrow launch with half the slots per lane, a quarter of the unrolled body
+// (the W = 16 narrow backward does not fit the instruction cache at one warp per SMSP) and each
+// coefficient shared by two packed column pairs (C2: backward 130 -> 101 us)
+enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16, M_NK4 = 32 };
 constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 
 __host__ __device__ constexpr int ring_warps(int mode) {
@@ -83,7 +87,8 @@ __host__ __device__ constexpr int kcols(int W, int mode) {
     // real columns per thread, so that the column state is ~128 registers (2 W K forward, 4 W K
     // backward); two packed fp32 columns per FFMA2 (one complex column in the unitary variant)
     const int k = ((mode & 3) == M_BWD) ? (32 / W > 8 ? 8 : 32 / W) : (64 / W > 8 ? 8 : 64 / W);
-    return ((mode & M_NARROW) && k > 2) ? 2 : k;
+    const int cap = (mode & M_NK4) ? 4 : 2;
+    return ((mode & M_NARROW) && k > cap) ? cap : k;
 }
 
 // ------------------------------------------------------------------ PTX helpers
@@ -873,7 +878,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                         if (lane == 0) mbar_arrive(&rfull[bi]);
                         grp++;
                     }
-                    if constexpr (r == RG / 2 - 1) {
+                    if constexpr (r == RG / 2 - 1 && NW > 4) {
+                        // (no high half in 4-warp CTAs: the call site would only cost instruction cache)
                         if (((warp >> 2) & 1) == 1 && grp >= 1) reduce_group(grp - 1);
                     }
                 }

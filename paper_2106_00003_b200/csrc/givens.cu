@@ -64,6 +64,7 @@ int fail(int code, const char *fmt, ...) {
 // ------------------------------------------------------------------ configuration
 struct Cfg {
     int ne, S, R, W, L, fast;  // fast: register ring kernel (else generic); L = instantiated lanes
+    int nk4 = 0;               // narrow launches use M_NK4 (4 columns per thread; W = 8 rings)
     int La;                    // active lanes per column group (S = W * La; La <= L)
     int rowbytes;              // bytes per table row (S float2, padded to 16)
 };
@@ -74,11 +75,12 @@ int dev_sms();
 int64_t cols_per_slab(const Cfg &c, int mode);
 
 // m: the batch the configuration will serve (real columns; -1 = unknown). The real ring at S = 128 /
-// 256 (n = 256 / 512) switches from W = 16 to W = 8 slots per lane (twice the lanes per column, so
-// twice the slabs) when the narrow W = 16 launch would leave more than half the SMs without a slab
-// -- the U-build and its gradient at those n (measured: n = 256 gradient 104 -> 72 us, n = 512
-// 201 -> 140 us), not C2 (128 slabs already; W = 8 would need two waves). Forward and backward of
-// one batch see the same m, hence the same configuration (the reuse tag checks it).
+// 256 (n = 256 / 512) runs W = 8 slots per lane instead of 16 whenever the W = 16 launch would be
+// narrow: with 2 columns per thread (twice the slabs) when the narrow W = 16 launch would leave more
+// than half the SMs without a slab -- the U-build and its gradient at those n (measured: n = 256
+// gradient 104 -> 72 us, n = 512 201 -> 140 us) -- else with 4 (M_NK4: the same slabs, a smaller
+// body; C2 backward 130 -> 101 us). Forward and backward of one batch see the same m, hence the same
+// configuration (the reuse tag checks it).
 Cfg make_cfg(int n, int64_t m = -1);
 Cfg make_cfg(int n, int64_t m) {
     Cfg c;
@@ -122,7 +124,12 @@ Cfg make_cfg(int n, int64_t m) {
         Cfg w8 = c;
         w8.W = 8; w8.L = w8.La = c.S / 8;
         const int64_t narrow16 = (m + cols_per_slab(c, M_FWD | M_NARROW) - 1) / cols_per_slab(c, M_FWD | M_NARROW);
+        const int64_t normal16 = (m + cols_per_slab(c, M_BWD) - 1) / cols_per_slab(c, M_BWD);
         if (2 * narrow16 <= dev_sms()) return w8;
+        if (normal16 < dev_sms()) {  // the W = 16 launches would be narrow (launch_mode)
+            w8.nk4 = 1;
+            return w8;
+        }
     }
     return c;
 }
@@ -176,8 +183,10 @@ int launch_mode(const Cfg &c, int mode, int64_t m) {
     const int H = c.L < 32 ? 1 : c.L / 32;
     if (H > 1) return mode;
     const int64_t slabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
-    const int64_t slabs_n = (m + cols_per_slab(c, mode | M_NARROW) - 1) / cols_per_slab(c, mode | M_NARROW);
-    return (slabs < dev_sms() && slabs_n > slabs) ? (mode | M_NARROW) : mode;
+    const int nm = mode | M_NARROW | (c.nk4 ? M_NK4 : 0);
+    const int64_t slabs_n = (m + cols_per_slab(c, nm) - 1) / cols_per_slab(c, nm);
+    if (!(slabs < dev_sms() && slabs_n > slabs)) return mode;
+    return mode | M_NARROW | (c.nk4 ? M_NK4 : 0);
 }
 
 // the generic backward keeps a private [vals][2S][S] fp32 partial per CTA; its grid is capped so

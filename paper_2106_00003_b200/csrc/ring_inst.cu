@@ -35,6 +35,12 @@ cudaError_t GK_CAT(ring_launch_, RING_W, RING_L)(int mode, const RingArgs &ra, i
         case M_BUILDU | M_NARROW: return launch_wlm<RING_W, RING_L, M_BUILDU | M_NARROW>(ra, grid, st);
         case M_TRANS | M_NARROW: return launch_wlm<RING_W, RING_L, M_TRANS | M_NARROW>(ra, grid, st);
         case M_BWD | M_NARROW: return launch_wlm<RING_W, RING_L, M_BWD | M_NARROW>(ra, grid, st);
+#if RING_W == 8  // 4 columns per thread (M_NK4)
+        case M_FWD | M_NARROW | M_NK4: return launch_wlm<RING_W, RING_L, M_FWD | M_NARROW | M_NK4>(ra, grid, st);
+        case M_BUILDU | M_NARROW | M_NK4: return launch_wlm<RING_W, RING_L, M_BUILDU | M_NARROW | M_NK4>(ra, grid, st);
+        case M_TRANS | M_NARROW | M_NK4: return launch_wlm<RING_W, RING_L, M_TRANS | M_NARROW | M_NK4>(ra, grid, st);
+        case M_BWD | M_NARROW | M_NK4: return launch_wlm<RING_W, RING_L, M_BWD | M_NARROW | M_NK4>(ra, grid, st);
+#endif
 #if GK_IDLE_CAPABLE
         case M_FWD | M_NARROW | M_IDLE: return launch_wlm<RING_W, RING_L, M_FWD | M_NARROW | M_IDLE>(ra, grid, st);
         case M_BUILDU | M_NARROW | M_IDLE:

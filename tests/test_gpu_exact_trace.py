@@ -166,3 +166,21 @@ def test_c3_rerun_bitwise(g):
     Ys = g.apply(tt, Xt[:, c0:c1].contiguous())
     _, xs = g.backward(tt, Ys, dYt[:, c0:c1].contiguous())
     assert torch.equal(Ys, Y1[:, c0:c1]) and torch.equal(xs, x1[:, c0:c1])
+
+
+@pytest.mark.parametrize("n,m", [(256, 4096), (512, 2048), (256, 256), (512, 512)])
+def test_exact_trace_latency_configs(g, n, m):
+    """The configurations chosen by batch size at n = 256 / 512 (W = 8 rings: 4 columns per thread at
+    C2-like m, 2 at U-build-like m; W = 16 otherwise), bit-exact like the rest."""
+    N = n * (n - 1) // 2
+    th = _angles(N, seed=n + m)
+    X = _ints(n, m, n + 1, synth.TID_X)
+    dY = _ints(n, m, n + 1, synth.TID_DY)
+    tt = _cuda(th)
+    X64, dY64 = X.astype(np.float64), dY.astype(np.float64)
+    Y = g.apply(tt, _cuda(X))
+    assert np.array_equal(Y.cpu().numpy(), _exact(oracle.apply(n, th, X64)))
+    dth, dX = g.backward(tt, Y, _cuda(dY))
+    dto, dXo = oracle.backward(n, th, X64, dY64)
+    assert np.array_equal(dX.cpu().numpy(), _exact(dXo))
+    assert np.array_equal(dth.cpu().numpy(), _exact(dto))

@@ -74,7 +74,7 @@ if os.path.exists(lp):
         for i, k, v in rows:
             f.write(f"{i},{k},{v:.0f}\n")
     tot = collections.Counter()
-    for _, k, v in rows[-8:]:  # one full step: 5 precompute + forward + backward + stage 2
+    for _, k, v in rows[-6:]:  # one full step: 3 precompute + forward + backward + stage 2
         tot[k] += v
     T = sum(tot.values())
     out["c3_step_share_from_launch_list"] = {k: {"ns": v, "share": round(v / T, 4)} for k, v in tot.items()}
