@@ -382,6 +382,36 @@ def step_reps(g, torch, theta, X, dY, n, reps=50, m_cols=None):
             "max_ms": max(t)}
 
 
+def fast_givens_line(g, torch, synth, dev, peak_tflops, n=64, m=1 << 20, reps=20):
+    """SURVEY §8(f4) measured beside the default: Y = U X at n = 64 (one-lane columns, where the
+    factoring choice of fast Givens is warp-uniform) by the three-shear ring (3 FFMA per
+    rotation-column) and by fast Givens (2 FFMA + the scaled store); device ms per call, mean of
+    `reps` back to back after warm-up, and each against the FP32 FLOP roofline (6 flops per
+    rotation-column)."""
+    N = n * (n - 1) // 2
+    th = torch.from_numpy(synth.theta(N, seed=SEED)).to(dev)
+    X = torch.from_numpy(synth.normal_matrix(n, m, SEED, synth.TID_X)).to(dev)
+    Y = torch.empty_like(X)
+    ws = g.workspace(g.OP_APPLY, n, m, dev)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    ts = timed(lambda: g.apply(th, X, out=Y, ws=ws))
+    tf = timed(lambda: g.fast_apply(th, X, out=Y, ws=ws))
+    fl = FLOPS_FWD * N * m
+    return {"workload": f"n={n}, m={m}: Y = U X (one-lane columns)", "three_shear_ms": round(ts, 4),
+            "fast_givens_ms": round(tf, 4), "three_shear_frac": fl / (ts * 1e-3) / 1e12 / peak_tflops,
+            "fast_givens_frac": fl / (tf * 1e-3) / 1e12 / peak_tflops, "speedup_fast_vs_three_shear": round(ts / tf, 3)}
+
+
 def _measured_peak(key, default):
     """A number from the driver-written MEASURED_PEAKS.json, else the stated fallback."""
     try:
@@ -638,6 +668,7 @@ def main():
             out["c2"] = small_config_line(g, torch, synth, dev)
             out["c5_shard"] = c5_shard_line(g, torch, synth, dev)
             out["unitary"] = unitary_line(g, torch, synth, dev, peak)
+            out["f4_fast_givens"] = fast_givens_line(g, torch, synth, dev, peak)
             bf16 = _measured_peak("bf16_tflops", 2250.0)
             out["f2_gemm_path"] = gemm_path_line(g, torch, theta, X, dY, n, m, ms_step, bf16 / 2)
         if world == 1 and not args.no_cpu_baseline:

@@ -223,6 +223,20 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
                          void *ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------------------------------
+ * Fast (square-root-free) Givens: the same Y = U(theta) X (and U) as
+ * givens_apply / givens_build_U, computed with two FMAs per rotation-column on scaled values
+ * x = d z, the per-row scales d and the choice between the two factorings (|cos| >= |sin|) made by
+ * the precompute. Only for one-lane columns (n_eff in {8, 16, 32, 64}: the factoring choice is then
+ * uniform across a warp), identity layout; GIVENS_EUNSUPPORTED for other n. Workspace: the
+ * GIVENS_OP_APPLY (resp. GIVENS_OP_BUILD_U) size; the tables it leaves are not reusable by a backward.
+ * A measured variant, not the default path.
+ * ------------------------------------------------------------------------------------------ */
+int givens_fast_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
+                      float *Y, int64_t ldy, void *ws, size_t ws_bytes, void *stream);
+int givens_fast_build_U(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu, void *ws,
+                        size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------------
  * GEMM path: the paper's own framing of the workload --
  * build U(theta) once (Alg. 2 from I on the register ring), then Y = U X (or U^T X) as a dense
  * GEMM on the tensor cores in 3xTF32 (hi/lo split of both operands, three TF32 products,

@@ -23,7 +23,7 @@ EXPORTS = [
     "givens_u_build_U", "givens_u_backward", "givens_check_perm", "givens_schedule_ex", "givens_mask_from_dims_ex",
     "givens_apply_ex", "givens_build_U_ex", "givens_backward_ex", "givens_u_apply_ex", "givens_u_build_U_ex",
     "givens_u_backward_ex", "givens_gemm_workspace_bytes", "givens_gemm_apply", "givens_gemm_backward",
-    "givens_workspace_reset",
+    "givens_workspace_reset", "givens_fast_apply", "givens_fast_build_U",
 ]
 
 
@@ -55,6 +55,10 @@ def lib():
         L.givens_schedule.argtypes = [I32, P, P]
         L.givens_mask_from_dims.restype = C
         L.givens_mask_from_dims.argtypes = [I32, P, P]
+        L.givens_fast_apply.restype = C
+        L.givens_fast_apply.argtypes = [I32, I64, P, P, P, I64, P, I64, P, SZ, P]
+        L.givens_fast_build_U.restype = C
+        L.givens_fast_build_U.argtypes = [I32, P, P, P, I64, P, SZ, P]
         L.givens_workspace_reset.restype = None
         L.givens_workspace_reset.argtypes = [P]
         L.givens_workspace_bytes.restype = SZ

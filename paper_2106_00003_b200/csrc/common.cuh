@@ -76,7 +76,12 @@ constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose 
 // slab width as the W = 16 narrow launch with half the slots per lane, a quarter of the unrolled body
 // (the W = 16 narrow backward does not fit the instruction cache at one warp per SMSP) and each
 // coefficient shared by two packed column pairs (C2: backward 130 -> 101 us)
-enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16, M_NK4 = 32 };
+// M_FG (forward / U-build on one-lane columns only): fast (square-root-free) Givens --
+// two FFMAs per rotation-column on scaled values z = x / d, the per-row scales d tracked by the
+// precompute (k_fg_tables), the factoring (unit coefficient on one input or the other) chosen per slot
+// by |cos| >= |sin|; warp-uniform in this layout because every lane holds a whole column
+enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16, M_NK4 = 32,
+            M_FG = 64 };
 constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 
 __host__ __device__ constexpr int ring_warps(int mode) {
@@ -155,6 +160,8 @@ struct RingArgs {
     float *partial;   // BWD: per CTA, per reduction group, NW warp blocks (see red_geom)
     int64_t nslabs;
     int vec_ok;       // 1 if all row starts are 16-byte aligned for K-wide vector access
+    const uint32_t *fgmask;  // M_FG: per table row, bit q = slot q uses the second factoring
+    const float *sfg;        // M_FG: final scale of each label (the store multiplies by it)
 };
 
 template <int K>
@@ -451,6 +458,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     // 6.99 ms; two-warp columns got slower (C5 shard forward 10.94 -> 11.63 ms), so they keep the
     // named barrier.
     constexpr bool DEFER = (H >= 4) && !GRAD;
+    constexpr bool FG = (MODE & M_FG) != 0;
+    static_assert(!FG || (L == 1 && !UNI && !GRAD && !UP), "fast Givens: forward / U-build on one-lane columns");
 
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem);
@@ -771,6 +780,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     __syncwarp();
                 }
                 const int srow = UP ? su : (SPS - 1 - su);
+                uint32_t fgm = 0;  // M_FG: this step's factoring bits (one table row, warp-uniform)
+                if constexpr (FG) fgm = __ldg(a.fgmask + stage_rho0(gst) + srow);
                 const uint8_t *sbase = stagebuf + (gst % NSTAGE) * G::STAGEB;
                 const float4 *row4 = reinterpret_cast<const float4 *>(sbase + srow * rowb);
                 const float4 *ph4 = reinterpret_cast<const float4 *>(sbase + SPS * rowb + srow * (G::PHB / 8) * rowb);
@@ -855,7 +866,16 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                                     ZT[p][q] = cmul4(ZT[p][q], pha);
                                     ZB[p][q] = cmul4(ZB[p][q], phb);
                                 }
-                                rot_fwd(ZT[p][q], ZB[p][q], tq, sq);
+                                if constexpr (FG) {
+                                    // (x, y) = (top, bottom) or, with the second factoring, (bottom, top):
+                                    // top' = x - a y, bottom' = y + b x (2 FFMA)
+                                    const bool fb = (fgm >> q) & 1u;
+                                    const V x = fb ? ZB[p][q] : ZT[p][q], y = fb ? ZT[p][q] : ZB[p][q];
+                                    ZT[p][q] = fma_v(-tq, y, x);
+                                    ZB[p][q] = fma_v(sq, x, y);
+                                } else {
+                                    rot_fwd(ZT[p][q], ZB[p][q], tq, sq);
+                                }
                             }
                         }
                     }
@@ -1038,6 +1058,24 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         }
         // ---------------- store from the end layout (s_{R-1} forward, s_0 backward)
         if (BM == M_BWD && a.Y == nullptr) continue;
+        if constexpr (FG) {
+            // y = d_final * z per row (identity layout only)
+#pragma unroll
+            for (int q = 0; q < W; q++) {
+                const int k = t * W + q;
+                const int lt = row_sRm1(k, ne), lb = row_sRm1(ne - 1 - k, ne);
+                V vt[KP], vb[KP];
+                const float st = lt < n ? __ldg(a.sfg + lt) : 0.f, sb = lb < n ? __ldg(a.sfg + lb) : 0.f;
+#pragma unroll
+                for (int p = 0; p < KP; p++) {
+                    vt[p] = mul_v(f2v<V>(st), ZT[p][q]);
+                    vb[p] = mul_v(f2v<V>(sb), ZB[p][q]);
+                }
+                if (active && lt < n) IO::store(a.Y + (int64_t)lt * a.ldy, col0, a.m, a.vec_ok, vt);
+                if (active && lb < n) IO::store(a.Y + (int64_t)lb * a.ldy, col0, a.m, a.vec_ok, vb);
+            }
+            continue;
+        }
         if (fast) {
 #pragma unroll
             for (int q = 0; q < W; q++) {

@@ -263,7 +263,7 @@ struct AutoWs {
 };
 
 struct WsLayout {
-    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, lay, partial, scratch, total;
+    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, lay, fgm, sfg, partial, scratch, total;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
@@ -286,6 +286,8 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     L.sig = off; off = al256(off + (size_t)c.R * c.ne);
     L.sfin = off; off = al256(off + (size_t)c.ne);
     L.lay = off; off = al256(off + (size_t)(c.ne + 2) * 4);
+    L.fgm = off; off = al256(off + rows * 4);            // fast Givens: factoring bits per table row
+    L.sfg = off; off = al256(off + (size_t)c.ne * 4);    // fast Givens: final scale per label
     L.partial = off;
     if (base == GIVENS_OP_BACKWARD) {
         int64_t g = grid_for(c, M_BWD | (uni ? M_UNI : 0), mr);
@@ -491,6 +493,64 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
     double cr = cos(thr), sr = sin(thr);
     if (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) sr = -sr;
     abr[pos_ab] = top_is_i ? make_float2((float)cr, (float)sr) : make_float2((float)sr, (float)cr);
+}
+
+// (3f) fast Givens tables (one-lane columns, S <= 32, identity layout). One CTA of S
+// threads walks the blocks in the forward's order (b_R first), thread k owning slot
+// k. The values are kept as x = d z with a per-label scale d (fp64 here, 1 at the start). In
+// (top, bottom) coordinates the block rotates by psi = theta (top holds the smaller row i) or -theta;
+// with c = cos psi, s = sin psi:
+//   |c| >= |s|: top' = c (u - (s/c) v), bottom' = c (v + (s/c) u):  z_t' = z_t - a z_b, z_b' = z_b + b z_t,
+//               a = (s/c) d_b / d_t, b = (s/c) d_t / d_b, d_t' = c d_t, d_b' = c d_b;
+//   |s| >  |c|: top' = -s (v - (c/s) u), bottom' = s (u + (c/s) v):  z_t' = z_b - a z_t, z_b' = z_t + b z_b,
+//               a = (c/s) d_t / d_b, b = (c/s) d_b / d_t, d_t' = -s d_b, d_b' = s d_t  (bit q of the row set).
+// The table row holds (a, b) where the three-shear table holds (t, s); masked / bye slots are the
+// identity (a = b = 0, scales unchanged). |a|, |b| <= 1 x the scale ratio; for n <= 64 the scales stay
+// within 2^-32 .. 1, so no renormalisation is needed.
+__global__ void k_fg_tables(int n, int ne, const float *__restrict__ theta, const uint8_t *__restrict__ mask,
+                            uint8_t *__restrict__ coef, int rowbytes, uint32_t *__restrict__ fgm,
+                            float *__restrict__ sfg) {
+    __shared__ double d[64];
+    __shared__ uint32_t bits;
+    const int S = ne / 2, R = ne - 1, k = threadIdx.x;
+    for (int l = k; l < ne; l += blockDim.x) d[l] = 1.0;
+    if (k < S) {  // pad rows: identity
+        reinterpret_cast<float2 *>(coef)[coef_pos(k, S, 1)] = make_float2(0.f, 0.f);
+        reinterpret_cast<float2 *>(coef + (int64_t)(R + 1) * rowbytes)[coef_pos(k, S, 1)] = make_float2(0.f, 0.f);
+    }
+    if (k == 0) fgm[0] = fgm[R + 1] = 0u;
+    __syncthreads();
+    for (int r = R - 1; r >= 0; r--) {  // forward order: b_R first
+        if (k == 0) bits = 0u;
+        __syncthreads();
+        if (k < S) {
+            const int la = seq_at(r, k, ne), lb = seq_at(r, ne - 1 - k, ne);
+            const int64_t f = flat_of(r, k, n, ne);
+            float2 ab = make_float2(0.f, 0.f);
+            if (f >= 0 && (!mask || mask[f])) {
+                const double th = remainder((double)theta[f], 6.283185307179586);
+                const double psi = la < lb ? th : -th;  // identity layout: label = row
+                const double c = cos(psi), sn = sin(psi), dt = d[la], db = d[lb];
+                if (fabs(c) >= fabs(sn)) {
+                    const double q = sn / c;
+                    ab = make_float2((float)(q * db / dt), (float)(q * dt / db));
+                    d[la] = c * dt;
+                    d[lb] = c * db;
+                } else {
+                    const double q = c / sn;
+                    ab = make_float2((float)(q * dt / db), (float)(q * db / dt));
+                    d[la] = -sn * db;
+                    d[lb] = sn * dt;
+                    atomicOr(&bits, 1u << k);
+                }
+            }
+            reinterpret_cast<float2 *>(coef + (int64_t)(r + 1) * rowbytes)[coef_pos(k, S, 1)] = ab;
+        }
+        __syncthreads();
+        if (k == 0) fgm[r + 1] = bits;
+    }
+    __syncthreads();
+    for (int l = k; l < ne; l += blockDim.x) sfg[l] = (float)d[l];
 }
 
 // ------------------------------------------------------------------ stage-2 dtheta reduction
@@ -958,6 +1018,8 @@ int run_apply_mode(int mode, int32_t n, int64_t m, const float *X, int64_t ldx, 
         ra.coef_ph = ws + ((mode & 3) == M_BWD ? L.coef_ph : ((mode & 3) == M_TRANS ? L.coef_pt : L.coef_pf));
         ra.coef_ab = ws + L.coef_ab;
         ra.partial = reinterpret_cast<float *>(ws + L.partial);
+        ra.fgmask = reinterpret_cast<const uint32_t *>(ws + L.fgm);
+        ra.sfg = reinterpret_cast<const float *>(ws + L.sfg);
         ra.nslabs = (m + cols_per_slab(c, mode) - 1) / cols_per_slab(c, mode);
         int K = kcols(c.W, mode);
         ra.vec_ok = vec_ok_for(K, {{X, ldx}, {dY, lddy}, {Y, ldy}});
@@ -1247,6 +1309,46 @@ int givens_u_backward(int32_t n, int64_t m, const float *theta, const float *phi
                       float *dtheta, float *dphi, int flags, void *ws, size_t ws_bytes, void *stream) {
     return givens_u_backward_ex(n, m, theta, phi, mask, Y, ldy, dY, lddy, dX, lddx, dtheta, dphi, flags, nullptr, -1,
                                 ws, ws_bytes, stream);
+}
+
+// ------------------------------------------------------------------ fast Givens
+namespace {
+int fast_common(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx, float *Y,
+                int64_t ldy, int mode, void *ws, size_t ws_bytes, cudaStream_t st) {
+    Cfg c = make_cfg(n, m);
+    if (!(c.fast && c.L == 1 && c.La == 1))
+        return fail(GIVENS_EUNSUPPORTED, "fast Givens runs on one-lane columns only (n_eff in {8, 16, 32, 64}; n = %d)", n);
+    WsLayout L = ws_layout(c, GIVENS_OP_APPLY, m);
+    AutoWs aw;
+    int rc;
+    if ((rc = aw.get(ws, ws_bytes, L.total, st))) return rc;
+    uint8_t *w = (uint8_t *)ws;
+    untag_tables(w);  // the tables below are not the three-shear ones a backward could reuse
+    k_fg_tables<<<1, 32, 0, st>>>(n, c.ne, theta, mask, w + L.coef, c.rowbytes, reinterpret_cast<uint32_t *>(w + L.fgm),
+                                  reinterpret_cast<float *>(w + L.sfg));
+    CUDA_TRY(cudaGetLastError());
+    return run_apply_mode(mode | M_FG, n, m, X, ldx, nullptr, 0, Y, ldy, w, L, c, st, nullptr);
+}
+}  // namespace
+
+int givens_fast_apply(int32_t n, int64_t m, const float *theta, const uint8_t *mask, const float *X, int64_t ldx,
+                      float *Y, int64_t ldy, void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_common(n, m, ws, ws_bytes, GIVENS_OP_APPLY);
+    if (rc) return rc;
+    if (!theta || (m > 0 && (!X || !Y))) return fail(GIVENS_EINVAL, "theta, X and Y must be non-NULL");
+    if (ldx < m || ldy < m) return fail(GIVENS_EINVAL, "leading dimension smaller than m");
+    if (X == Y && ldx != ldy) return fail(GIVENS_EINVAL, "in-place apply needs ldx == ldy");
+    if (m == 0) return make_cfg(n).L == 1 && make_cfg(n).fast ? 0 : fail(GIVENS_EUNSUPPORTED, "fast Givens: n = %d", n);
+    return fast_common(n, m, theta, mask, X, ldx, Y, ldy, M_FWD, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int givens_fast_build_U(int32_t n, const float *theta, const uint8_t *mask, float *U, int64_t ldu, void *ws,
+                        size_t ws_bytes, void *stream) {
+    int rc = check_common(n, n, ws, ws_bytes, GIVENS_OP_BUILD_U);
+    if (rc) return rc;
+    if (!theta || !U) return fail(GIVENS_EINVAL, "theta and U must be non-NULL");
+    if (ldu < n) return fail(GIVENS_EINVAL, "ldu < n");
+    return fast_common(n, n, theta, mask, nullptr, 0, U, ldu, M_BUILDU, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int givens_index_trace(int32_t n, int direction, int32_t *out_dev, void *stream) {

@@ -26,6 +26,9 @@ __device__ __forceinline__ float2 fma_v(float a, float2 b, float2 c) { return __
 __device__ __forceinline__ float2 fma_v(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 
 __device__ __forceinline__ float mul_v(float a, float b) { return a * b; }
+template <typename V> __device__ __forceinline__ V f2v(float a);
+template <> __device__ __forceinline__ float f2v<float>(float a) { return a; }
+template <> __device__ __forceinline__ float2 f2v<float2>(float a) { return make_float2(a, a); }
 __device__ __forceinline__ float2 mul_v(float2 a, float2 b) { return __fmul2_rn(a, b); }
 __device__ __forceinline__ float neg_v(float a) { return -a; }
 __device__ __forceinline__ float2 neg_v(float2 a) { return make_float2(-a.x, -a.y); }

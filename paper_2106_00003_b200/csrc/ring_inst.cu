@@ -61,6 +61,12 @@ cudaError_t GK_CAT(ring_launch_, RING_W, RING_L)(int mode, const RingArgs &ra, i
         case M_BWD | M_UNI | M_IDLE: return launch_wlm<RING_W, RING_L, M_BWD | M_UNI | M_IDLE>(ra, grid, st);
 #endif
 #endif
+#if RING_L == 1  // fast Givens: forward and U-build on one-lane columns
+        case M_FWD | M_FG: return launch_wlm<RING_W, RING_L, M_FWD | M_FG>(ra, grid, st);
+        case M_BUILDU | M_FG: return launch_wlm<RING_W, RING_L, M_BUILDU | M_FG>(ra, grid, st);
+        case M_FWD | M_FG | M_NARROW: return launch_wlm<RING_W, RING_L, M_FWD | M_FG | M_NARROW>(ra, grid, st);
+        case M_BUILDU | M_FG | M_NARROW: return launch_wlm<RING_W, RING_L, M_BUILDU | M_FG | M_NARROW>(ra, grid, st);
+#endif
         case M_FWD: return launch_wlm<RING_W, RING_L, M_FWD>(ra, grid, st);
         case M_BUILDU: return launch_wlm<RING_W, RING_L, M_BUILDU>(ra, grid, st);
         case M_TRANS: return launch_wlm<RING_W, RING_L, M_TRANS>(ra, grid, st);

@@ -225,6 +225,38 @@ def backward(theta: torch.Tensor, Y: torch.Tensor, dY: torch.Tensor, mask: torch
     return dtheta, dX
 
 
+# ---------------------------------------------------------------- fast Givens
+
+@_on_device
+def fast_apply(theta, X, mask=None, out=None, ws=None):
+    """Y = U(theta) X by fast (square-root-free) Givens: 2 FMAs per rotation-column on scaled values
+    (n_eff in {8, 16, 32, 64} only)."""
+    n, m = X.shape
+    _check_matrix("X", X, n)
+    _check_theta(theta, mask, n)
+    Y = torch.empty_like(X) if out is None else out
+    _check_matrix("out", Y, n)
+    _same_shape("out", Y, X)
+    if ws is None:
+        ws = workspace(OP_APPLY, n, m, X.device)
+    check(lib().givens_fast_apply(n, m, _ptr(theta), _ptr(mask), _ptr(X), X.stride(0), _ptr(Y), Y.stride(0),
+                                  _ptr(ws), ws.numel(), _stream(X.device)))
+    return Y
+
+
+@_on_device
+def fast_build_U(theta, n: int, mask=None, out=None, ws=None):
+    """U = U(theta) by fast Givens (n_eff in {8, 16, 32, 64} only)."""
+    _check_theta(theta, mask, n)
+    U = torch.empty((n, n), dtype=torch.float32, device=theta.device) if out is None else out
+    _check_matrix("U", U, n)
+    if ws is None:
+        ws = workspace(OP_BUILD_U, n, n, theta.device)
+    check(lib().givens_fast_build_U(n, _ptr(theta), _ptr(mask), _ptr(U), U.stride(0), _ptr(ws), ws.numel(),
+                                    _stream(theta.device)))
+    return U
+
+
 # ---------------------------------------------------------------- GEMM path (SURVEY §8(f2))
 
 def gemm_workspace(n: int, m: int, device=None) -> torch.Tensor:
