@@ -83,6 +83,9 @@ constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose 
 enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16, M_NK4 = 32,
             M_FG = 64 };
 constexpr int kNWN = 4;  // warps per CTA of the narrow variant
+#ifndef GK_BWD_IL
+#define GK_BWD_IL 1  // interleave the replays of a slot pair in the real backward (C3 bwd 15.78 -> 15.60 ms)
+#endif
 
 __host__ __device__ constexpr int ring_warps(int mode) {
     return (mode & M_NARROW) ? kNWN : ((mode & 3) == 3 ? kNW : kNWF);
@@ -813,6 +816,16 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     const float4 cf = row4[pp * La + tc];
                     float4 ab = make_float4(0.f, 0.f, 0.f, 0.f);
                     if constexpr (GRAD && UNI) ab = ab4[pp * La + tc];
+                    // real backward, one packed pair per slot: both slots' cross products first, then the
+                    // two slots' replays interleaved (four independent FFMA2 chains per shear)
+                    constexpr bool IL = GRAD && !UNI && KP == 1 && H < 4 && GK_BWD_IL;  // (four-warp columns: 22.9 -> 23.2 ms, off)
+                    if constexpr (IL) {
+                        const int q0 = 2 * pp, q1 = q0 + 1;
+                        acc[LC > 1 ? q0 : (q0 & 3)] = cross_first(DB[0][q0], ZT[0][q0], DT[0][q0], ZB[0][q0]);
+                        acc[LC > 1 ? q1 : (q1 & 3)] = cross_first(DB[0][q1], ZT[0][q1], DT[0][q1], ZB[0][q1]);
+                        rot_inv2x2(ZT[0][q0], ZB[0][q0], DT[0][q0], DB[0][q0], ZT[0][q1], ZB[0][q1], DT[0][q1], DB[0][q1],
+                                   cf.x, cf.y, cf.z, cf.w);
+                    } else {
 #pragma unroll
                     for (int hh = 0; hh < 2; hh++) {
                         const int q = 2 * pp + hh;
@@ -879,6 +892,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                             }
                         }
                     }
+                    }  // IL
                     if constexpr (GRAD && LC == 1) {
                         // one lane per column group and warp: the per-slot sums go straight to the ring
                         if (pp & 1) {

@@ -101,6 +101,24 @@ __device__ __forceinline__ void rot_inv2(V &x, V &y, V &u, V &v, float tq, float
     u = fma_v(tq, v, u);
 }
 
+// Two slots' replays interleaved: four independent chains per shear stage.
+template <typename V>
+__device__ __forceinline__ void rot_inv2x2(V &x0, V &y0, V &u0, V &v0, V &x1, V &y1, V &u1, V &v1, float t0,
+                                           float s0, float t1, float s1) {
+    x0 = fma_v(t0, y0, x0);
+    u0 = fma_v(t0, v0, u0);
+    x1 = fma_v(t1, y1, x1);
+    u1 = fma_v(t1, v1, u1);
+    y0 = fma_v(-s0, x0, y0);
+    v0 = fma_v(-s0, u0, v0);
+    y1 = fma_v(-s1, x1, y1);
+    v1 = fma_v(-s1, u1, v1);
+    x0 = fma_v(t0, y0, x0);
+    u0 = fma_v(t0, v0, u0);
+    x1 = fma_v(t1, y1, x1);
+    u1 = fma_v(t1, v1, u1);
+}
+
 // ---- the ring shift ------------------------------------------------------------------------
 // s_r -> s_{r+1} (backward / transpose direction): positions p -> p+1 on the ring 1..n_eff-1.
 template <int W, typename V>
