@@ -83,6 +83,9 @@ constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose 
 enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16, M_NK4 = 32,
             M_FG = 64 };
 constexpr int kNWN = 4;  // warps per CTA of the narrow variant
+#ifndef GK_UNI_ONE_SITE
+#define GK_UNI_ONE_SITE 1  // unitary backward: one reduction call site per group (u_backward 63.3 -> 62.5 ms)
+#endif
 #ifndef GK_BWD_IL
 #define GK_BWD_IL 1  // interleave the replays of a slot pair in the real backward (C3 bwd 15.78 -> 15.60 ms)
 #endif
@@ -951,15 +954,18 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     // LO = RG - 2 (not the group's last step) leaves the low half a step of slack
                     // before the next group's rempty wait (C3 bwd 15.74 -> 15.63 ms)
                     constexpr int LO = RG >= 4 ? RG - 2 : RG - 1;
+                    // ONE_SITE: every warp reduces at step LO (one inlined copy of the reduction per group
+                    // instead of two: the unitary backward's body does not fit the instruction cache)
+                    constexpr bool ONE_SITE = UNI && GK_UNI_ONE_SITE;
                     if constexpr (r == LO) {
-                        if (((warp >> 2) & 1) == 0 && grp >= 1) reduce_group(grp - 1);
+                        if ((ONE_SITE || ((warp >> 2) & 1) == 0) && grp >= 1) reduce_group(grp - 1);
                     }
                     if constexpr (r == RG - 1) {
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&rfull[bi]);
                         grp++;
                     }
-                    if constexpr (r == RG / 2 - 1 && NW > 4) {
+                    if constexpr (r == RG / 2 - 1 && NW > 4 && !ONE_SITE) {
                         // (no high half in 4-warp CTAs: the call site would only cost instruction cache)
                         if (((warp >> 2) & 1) == 1 && grp >= 1) reduce_group(grp - 1);
                     }
