@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -124,7 +125,7 @@ constexpr int CL = 2;
 
 template <bool AMN, bool BMN>
 __global__ void __cluster_dims__(1, CL, 1) __launch_bounds__(NTHREADS, 1)
-k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Args a) {
+k_gemm3_1sm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Args a) {
     extern __shared__ uint8_t smem_raw[];
     // SWIZZLE_128B atoms need 1024-byte alignment
     uint8_t *smem = reinterpret_cast<uint8_t *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -299,6 +300,204 @@ k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUten
 
 }  // namespace tcg
 
+namespace tcg {
+
+// ------------------------------------------------------------------ two-SM (cta_group::2) variant
+// A CTA pair (cluster along M) computes a 256 x 256 tile: each CTA holds its own 128 rows of A and
+// one 128-row half of B in shared memory (raw + lo, 64 KB per stage, three stages); the even CTA's
+// single elected thread issues tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8), which reads A and
+// B from both CTAs' shared memory and accumulates each CTA's 128 rows into that CTA's TMEM. Per CTA
+// the tensor core reads half the B bytes of the one-SM kernel. Both CTAs' split warps arrive on the
+// leader's conversion barrier (remote arrive, cluster scope); the leader's commits multicast to both
+// CTAs' stage-empty and accumulator barriers.
+constexpr int BN2 = 256, TILE_B2 = (BN2 / 2) * BK * 4;             // 16 KB: this CTA's half of B
+constexpr int HI2 = TILE_A + TILE_B2, STAGE2 = 2 * HI2, NST2 = 3;  // 64 KB per stage
+constexpr size_t SMEM2 = 1024 + (size_t)NST2 * STAGE2 + 256;
+
+template <bool AMN, bool BMN>
+__host__ __device__ constexpr uint32_t idesc_tf32_2sm() {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((AMN ? 1u : 0u) << 15) | ((BMN ? 1u : 0u) << 16) |
+           ((uint32_t)(BN2 >> 3) << 17) | ((uint32_t)((2 * BM) >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32_2sm(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_2sm(uint64_t *bar, uint16_t ctamask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(gk::smem_u32(bar)), "h"(ctamask)
+                 : "memory");
+}
+// arrive on the barrier at this shared-memory offset in CTA `rank` of the cluster (release, cluster scope)
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank) {
+    uint32_t raddr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(raddr) : "r"(gk::smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *b, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(gk::smem_u32(b)), "r"(parity)
+            : "memory");
+    }
+}
+
+// grid (2 x N tiles, M tile pairs, K splits), clusters of 2 along x: x = 2 n_tile + rank, so the CTA
+// pairs of all N tiles of one M pair run together (the streamed A tile comes from DRAM once)
+template <bool AMN, bool BMN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+k_gemm3(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, const Args a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)NST2 * STAGE2);
+    uint64_t *conv = full + NST2;
+    uint64_t *empty = conv + NST2;
+    uint64_t *accb = empty + NST2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accb + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = cluster_rank();
+    const int n0 = (blockIdx.x >> 1) * BN2, m0 = (blockIdx.y * 2 + (int)crank) * BM;  // this CTA's 128 of 256 rows
+    const int kbeg = blockIdx.z * a.kchunk;
+    const int kend = min(a.K, kbeg + a.kchunk);
+    const int nkb = (kend - kbeg + BK - 1) / BK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST2; s++) {
+            gk::mbar_init(&full[s], 1);
+            gk::mbar_init(&conv[s], 8);  // the split warps of both CTAs (used in the even CTA)
+            gk::mbar_init(&empty[s], 1);
+        }
+        gk::mbar_init(accb, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        gk::fence_proxy_async_smem();
+    }
+    if (warp == 2) {  // TMEM of each CTA of the pair: 256 fp32 columns x 128 lanes
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gk::smem_u32(tmem_slot)),
+                     "n"(BN2));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+            for (int kb = 0; kb < nkb; kb++) {
+                const int s = kb % NST2, j = kb / NST2;
+                if (j > 0) gk::mbar_wait(&empty[s], (uint32_t)((j - 1) & 1));
+                uint8_t *st = smem + (size_t)s * STAGE2;
+                gk::mbar_expect_tx(&full[s], HI2);
+                const int k0 = kbeg + kb * BK;
+                if constexpr (AMN) {
+#pragma unroll
+                    for (int b = 0; b < BM / 32; b++) tma_load_2d(st + b * 4096, &tma_a, m0 + 32 * b, k0, &full[s]);
+                } else {
+                    tma_load_2d(st, &tma_a, k0, m0, &full[s]);
+                }
+                const int nh = n0 + (int)crank * (BN2 / 2);  // this CTA's half of the N tile
+                if constexpr (BMN) {
+#pragma unroll
+                    for (int b = 0; b < BN2 / 2 / 32; b++)
+                        tma_load_2d(st + TILE_A + b * 4096, &tma_b, nh + 32 * b, k0, &full[s]);
+                } else {
+                    tma_load_2d(st + TILE_A, &tma_b, k0, nh, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && crank == 0) {
+            constexpr uint32_t idesc = idesc_tf32_2sm<AMN, BMN>();
+            const uint32_t base = gk::smem_u32(smem);
+            for (int kb = 0; kb < nkb; kb++) {
+                const int s = kb % NST2, j = kb / NST2;
+                mbar_wait_cluster(&conv[s], (uint32_t)(j & 1));
+                tc_fence_after();
+                const uint32_t ahi = base + s * STAGE2, bhi = ahi + TILE_A;
+                const uint32_t alo = ahi + HI2, blo = bhi + HI2;
+#pragma unroll
+                for (int ks = 0; ks < BK / 8; ks++) {
+                    const uint64_t dah = odesc<AMN>(ahi, ks), dal = odesc<AMN>(alo, ks);
+                    const uint64_t dbh = odesc<BMN>(bhi, ks), dbl = odesc<BMN>(blo, ks);
+                    const uint32_t acc0 = (kb > 0 || ks > 0) ? 1u : 0u;
+                    mma_tf32_2sm(tmem, dah, dbl, idesc, acc0);
+                    mma_tf32_2sm(tmem, dal, dbh, idesc, 1u);
+                    mma_tf32_2sm(tmem, dah, dbh, idesc, 1u);
+                }
+                mma_commit_2sm(&empty[s], 3);  // frees stage s in both CTAs once these MMAs have read it
+            }
+            mma_commit_2sm(accb, 3);  // both CTAs' accumulators are complete
+        }
+    } else if (warp >= 4) {
+        const int t = threadIdx.x - 128;
+        for (int kb = 0; kb < nkb; kb++) {
+            const int s = kb % NST2, j = kb / NST2;
+            gk::mbar_wait(&full[s], (uint32_t)(j & 1));
+            float4 *hi = reinterpret_cast<float4 *>(smem + (size_t)s * STAGE2);
+            float4 *lo = reinterpret_cast<float4 *>(smem + (size_t)s * STAGE2 + HI2);
+#pragma unroll 4
+            for (int i = t; i < HI2 / 16; i += 128) {
+                const float4 x = hi[i];
+                lo[i] = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+            }
+            gk::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(&conv[s], 0);  // the even CTA issues the MMAs
+        }
+        const int q = warp & 3;
+        gk::mbar_wait(accb, 0);
+        tc_fence_after();
+        const int mrow = m0 + 32 * q + lane;
+        float *outz = a.out + (int64_t)blockIdx.z * a.zstride;
+#pragma unroll 1
+        for (int c = 0; c < BN2; c += 32) {
+            uint32_t v[32];
+            const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c;
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                  "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+                  "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+                  "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+                  "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (mrow < a.M) {
+#pragma unroll
+                for (int jj = 0; jj < 32; jj++) {
+                    const int nn = n0 + c + jj;
+                    if (nn < a.N) {
+                        float *o = outz + (int64_t)nn * a.ldo + mrow;
+                        *o = a.accumulate ? *o + __uint_as_float(v[jj]) : __uint_as_float(v[jj]);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(BN2));
+    }
+}
+
+}  // namespace tcg
+
 // ------------------------------------------------------------------ host side
 namespace tcg {
 
@@ -354,17 +553,32 @@ template <bool AMN, bool BMN>
 inline cudaError_t gemm3_launch(const Operand &A, const Operand &B, int M, int N, int K, int kchunk, float *out,
                                 int64_t ldo, int64_t zstride, int accumulate, cudaStream_t st) {
     CUtensorMap ma, mb;
+    // the B map's box is half an N tile in both kernels (BN / CL = BN2 / 2 = 128 rows)
     if (!make_map(&ma, A.p, M, K, A.ld, AMN, BM) || !make_map(&mb, B.p, N, K, B.ld, BMN, BN / CL))
         return cudaErrorNotSupported;
-    static bool attr = [] {
-        return cudaFuncSetAttribute(k_gemm3<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) ==
-               cudaSuccess;
+    static const bool one_sm = [] {
+        const char *e = getenv("GIVENS_TC_1SM");
+        return e && atoi(e) != 0;
     }();
-    if (!attr) return cudaErrorInvalidConfiguration;
     Args a{M, N, K, kchunk, out, ldo, zstride, accumulate};
     const int mt = (M + BM - 1) / BM;  // M tiles, padded to whole clusters (a padding CTA loads zeros, stores nothing)
-    dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((mt + CL - 1) / CL * CL), (unsigned)((K + kchunk - 1) / kchunk));
-    k_gemm3<AMN, BMN><<<grid, NTHREADS, SMEM_BYTES, st>>>(ma, mb, a);
+    if (one_sm) {
+        static bool attr = [] {
+            return cudaFuncSetAttribute(k_gemm3_1sm<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)SMEM_BYTES) == cudaSuccess;
+        }();
+        if (!attr) return cudaErrorInvalidConfiguration;
+        dim3 grid((unsigned)((N + BN - 1) / BN), (unsigned)((mt + CL - 1) / CL * CL), (unsigned)((K + kchunk - 1) / kchunk));
+        k_gemm3_1sm<AMN, BMN><<<grid, NTHREADS, SMEM_BYTES, st>>>(ma, mb, a);
+        return cudaGetLastError();
+    }
+    static bool attr2 = [] {
+        return cudaFuncSetAttribute(k_gemm3<AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM2) ==
+               cudaSuccess;
+    }();
+    if (!attr2) return cudaErrorInvalidConfiguration;
+    dim3 grid((unsigned)(2 * ((N + BN2 - 1) / BN2)), (unsigned)((mt + 1) / 2), (unsigned)((K + kchunk - 1) / kchunk));
+    k_gemm3<AMN, BMN><<<grid, NTHREADS, SMEM2, st>>>(ma, mb, a);
     return cudaGetLastError();
 }
 
