@@ -312,3 +312,29 @@ def test_host_pipeline_matches_direct(g):
         Y = g.apply(tt, _cuda(batches[k][0]))
         want, _ = g.backward(tt, Y, _cuda(batches[k][1]), want_dX=False)
         assert torch.equal(got, want.cpu())
+
+
+def test_c5_shard_full_launch(g):
+    """C5 as one rank of its 8-GPU run, in the bench launch configuration: n = 2047 (odd: the bye),
+    32768 columns, the §5 mask m_keep = 1024. Y and dX on sampled columns vs the oracle, pinned angles
+    exactly 0, dtheta of the first block vs its closed form (Y dY^T - dY Y^T)_{ij} (pinned entries 0),
+    and shard additivity dtheta(A u B) = dtheta(A) + dtheta(B)."""
+    n, m = 2047, 32768
+    th, X, dY, mask = _inputs(n, m, seed=17, mask_keep=1024)
+    tt, Xt, dYt, mt = _cuda(th), _cuda(X), _cuda(dY), _cuda(mask)
+    Y = g.apply(tt, Xt, mask=mt)
+    dth, dX = g.backward(tt, Y, dYt, mask=mt)
+    d = dth.cpu().numpy()
+    assert (d[mask == 0] == 0).all()
+    cols = np.unique(np.concatenate([np.arange(3), np.random.default_rng(5).integers(0, m, 9), [m - 1]]))
+    Xs, dYs = X[:, cols].astype(np.float64), dY[:, cols].astype(np.float64)
+    assert rel(Y.cpu().numpy()[:, cols], oracle.apply(n, th, Xs, mask=mask)) <= TOL_Y
+    _, dXo = oracle.backward(n, th, Xs, dYs, mask=mask)
+    assert rel(dX.cpu().numpy()[:, cols], dXo) <= TOL_Y
+    f, want = _closed_form_block_dtheta(g, n, Y, dYt, 0)
+    want = np.where(mask[f] == 0, 0.0, want)
+    assert rel(d[f], want) <= TOL_DTH
+    h = 12288
+    d1, _ = g.backward(tt, Y[:, :h].contiguous(), dYt[:, :h].contiguous(), mask=mt, want_dX=False)
+    d2, _ = g.backward(tt, Y[:, h:].contiguous(), dYt[:, h:].contiguous(), mask=mt, want_dX=False)
+    assert rel((d1 + d2).cpu().numpy(), d) <= 1e-5
