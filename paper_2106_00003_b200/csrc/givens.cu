@@ -554,30 +554,26 @@ __global__ void k_fg_tables(int n, int ne, const float *__restrict__ theta, cons
 }
 
 // ------------------------------------------------------------------ stage-2 dtheta reduction
-// dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in a fixed order (PAPER.md:768-781
-// "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0. A CTA handles 32
-// consecutive table slots x 8 CTA phases: thread (x, y) sums the CTAs y, y + 8, y + 16, ... in
-// increasing order (eight independent load chains instead of one G-long one, each warp reading 32
-// consecutive floats), then row y = 0 adds the eight phase sums in order 0..7.
-constexpr int kRedPh = 8;
-__global__ void __launch_bounds__(32 * kRedPh) k_dtheta_reduce(int S, int W, int L, int NW, int G, int ring, int vals,
-                                                               const float *__restrict__ partial,
-                                                               const int32_t *__restrict__ amap,
-                                                               float *__restrict__ dtheta, float *__restrict__ dphi) {
-    __shared__ float ph[kRedPh][32];
-    const int64_t idx = (int64_t)blockIdx.x * 32 + threadIdx.x;
-    const int rows = 2 * S, y = threadIdx.y;
-    const bool in = idx < (int64_t)rows * S;
-    const int32_t code = in ? amap[idx] : -1;
-    const int64_t f = code & 0x1FFFFFFF;
-    const bool live = code >= 0 && !(code & (1 << 29));
-    if (code >= 0 && (code & (1 << 29)) && y == 0) {
+// dtheta[flat] = sgn * sum_{cta = 0..G-1} partial[cta][rho][k] in fixed CTA order (PAPER.md:768-781
+// "d <- A 1", made deterministic: no atomics). Masked angles get exactly 0. One thread per table slot
+// summing the G CTAs in order (measured against an eight-phase variant and a memory-order variant in
+// round 2: this one was fastest at every size -- C3 100 vs 179 us, C4 1.33 vs 2.58 ms under ncu).
+__global__ void k_dtheta_reduce(int S, int W, int L, int NW, int G, int ring, int vals, const float *__restrict__ partial,
+                                const int32_t *__restrict__ amap, float *__restrict__ dtheta, float *__restrict__ dphi) {
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int rows = 2 * S;
+    if (idx >= (int64_t)rows * S) return;
+    int32_t code = amap[idx];
+    if (code < 0) return;
+    int64_t f = code & 0x1FFFFFFF;
+    if (code & (1 << 29)) {
         dtheta[f] = 0.f;
         if (vals > 1) dphi[f] = 0.f;
+        return;
     }
-    const int rho = in ? (int)(idx / S) : 0, k = in ? (int)(idx % S) : 0;
+    int rho = (int)(idx / S), k = (int)(idx % S);
     for (int v = 0; v < vals; v++) {
-        int64_t pos = 0, stride = 0;
+        int64_t pos, stride;
         if (ring) {
             // ring kernel layout: per CTA, per group of RG steps, NW warp blocks of RG x OUTCH float4;
             // slot k (lane t = k / W of the group, slot q = k % W) is chunk ci = v*NCHW1 + (q/4)*LW + t%LW
@@ -597,21 +593,11 @@ __global__ void __launch_bounds__(32 * kRedPh) k_dtheta_reduce(int S, int W, int
             pos = ((int64_t)v * rows + rho) * S + k;  // generic kernel: natural order, [vals][rows][S]
             stride = (int64_t)vals * rows * S;
         }
-        float sp = 0.f;
-        if (live) {
-            const float *p = partial + pos;
-            for (int cc = y; cc < G; cc += kRedPh) sp += p[(int64_t)cc * stride];
-        }
-        ph[y][threadIdx.x] = sp;
-        __syncthreads();
-        if (y == 0 && live) {
-            float s2 = ph[0][threadIdx.x];
-#pragma unroll
-            for (int jj = 1; jj < kRedPh; jj++) s2 += ph[jj][threadIdx.x];
-            if (v == 0) dtheta[f] = (code & (1 << 30)) ? -s2 : s2;
-            else dphi[f] = s2;  // dphi carries no sign: sigma_i^2 = 1
-        }
-        __syncthreads();
+        float s = 0.f;
+        const float *p = partial + pos;
+        for (int cc = 0; cc < G; cc++) s += p[(int64_t)cc * stride];
+        if (v == 0) dtheta[f] = (code & (1 << 30)) ? -s : s;
+        else dphi[f] = s;  // dphi carries no sign: sigma_i^2 = 1
     }
 }
 
@@ -1199,8 +1185,8 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
     }
     if ((rc = run_apply_mode(M_BWD | M_UNI, n, 2 * m, Y, 2 * ldy, dY, 2 * lddy, dX, 2 * lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD | M_UNI, 2 * m);
-    int64_t tot = (int64_t)2 * c.S * c.S;
-    k_dtheta_reduce<<<(unsigned)((tot + 31) / 32), dim3(32, kRedPh), 0, st>>>(
+    const int64_t tot = (int64_t)2 * c.S * c.S;
+    k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
         c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD | M_UNI, 2 * m)), (int)G, c.fast, 2,
         reinterpret_cast<const float *>(w + L.partial),
         reinterpret_cast<const int32_t *>(w + L.amap), dtheta, dphi);
@@ -1272,8 +1258,8 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
     }
     if ((rc = run_apply_mode(M_BWD, n, m, Y, ldy, dY, lddy, dX, lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD, m);
-    int64_t tot = (int64_t)2 * c.S * c.S;
-    k_dtheta_reduce<<<(unsigned)((tot + 31) / 32), dim3(32, kRedPh), 0, st>>>(
+    const int64_t tot = (int64_t)2 * c.S * c.S;
+    k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
         c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD, m)), (int)G, c.fast, 1,
         reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
         dtheta, nullptr);
