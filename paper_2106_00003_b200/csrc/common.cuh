@@ -83,6 +83,9 @@ constexpr int kNWF = GK_FWD_WARPS;  // warps per CTA of the forward / transpose 
 enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE = 8, M_NARROW = 16, M_NK4 = 32,
             M_FG = 64 };
 constexpr int kNWN = 4;  // warps per CTA of the narrow variant
+#ifndef GK_HALF_BODY
+#define GK_HALF_BODY 0  // bit mask (1 unitary bwd, 2 unitary fwd, 4 real bwd, 8 real fwd): W/2-step bodies
+#endif
 #ifndef GK_UNI_ONE_SITE
 #define GK_UNI_ONE_SITE 1  // unitary backward: one reduction call site per group (u_backward 63.3 -> 62.5 ms)
 #endif
@@ -464,6 +467,11 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     // 6.99 ms; two-warp columns got slower (C5 shard forward 10.94 -> 11.63 ms), so they keep the
     // named barrier.
     constexpr bool DEFER = (H >= 4) && !GRAD;
+    constexpr int UBH = W / 2;
+    constexpr bool HALF = ((UNI && GRAD && (GK_HALF_BODY & 1)) || (UNI && !GRAD && (GK_HALF_BODY & 2)) ||
+                           (!UNI && GRAD && (GK_HALF_BODY & 4)) || (!UNI && !GRAD && (GK_HALF_BODY & 8))) &&
+                          UBH % G::SPS == 0 && (!GRAD || UBH % G::RG == 0) && UBH % 2 == 0;
+    constexpr int UB = HALF ? UBH : W;  // steps per unrolled body
     constexpr bool FG = (MODE & M_FG) != 0;
     static_assert(!FG || (L == 1 && !UNI && !GRAD && !UP), "fast Givens: forward / U-build on one-lane columns");
 
@@ -775,10 +783,12 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             }
         }
 
-        // ---------------- all 2S steps, W steps per unrolled body (register renaming of the ring)
+        // ---------------- all 2S steps, UB steps per unrolled body (register renaming of the ring:
+        // a body of W steps returns every ring register to its place; UB = W/2 leaves the renaming
+        // half way round, and the compiler moves the ring registers at the loop edge)
 #pragma unroll 1
-        for (int body = 0; body < STEPS / W; body++) {
-            unroll<W>([&](auto ic) {
+        for (int body = 0; body < STEPS / UB; body++) {
+            unroll<UB>([&](auto ic) {
                 constexpr int uu = decltype(ic)::value;
                 constexpr int su = uu % SPS;
                 if constexpr (su == 0) {
@@ -1072,7 +1082,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         if constexpr (DEFER) {
             if (xpend) {  // the last step's exchange
                 mbar_wait(&xb[cw], (uint32_t)((xn - 1) & 1));
-                xpatch((W - 1) & 1);
+                xpatch((UB - 1) & 1);
                 xpend = false;
             }
         }
