@@ -649,8 +649,8 @@ def main():
             "bwd_ms": ms_bwd, "fwd_ms": ms_step - ms_bwd, "step_ms_stats_rank0": step_stats,
             # forward-only (precompute + forward) and backward-only (replay + stage 2) rates
             "fwd_rotations_per_s": units / ((ms_step - ms_bwd) * 1e-3), "bwd_rotations_per_s": units / (ms_bwd * 1e-3),
-            # our kernels per step: k_flip, k_sigma, k_coef (precompute), forward, backward, stage-2 reduce
-            "gpu_launches": 6 * args.steps,
+            # our kernels per step: k_sigma_bits, k_coef (precompute), forward, backward, stage-2 reduce
+            "gpu_launches": 5 * args.steps,
             "clocks": clk,
         }
         if e2e:

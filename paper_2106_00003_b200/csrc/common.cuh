@@ -89,6 +89,9 @@ constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #ifndef GK_UNI_ONE_SITE
 #define GK_UNI_ONE_SITE 1  // unitary backward: one reduction call site per group (u_backward 63.3 -> 62.5 ms)
 #endif
+#ifndef GK_NO_PARTIAL
+#define GK_NO_PARTIAL 0  // timing ablation only (wrong dtheta): skip the bulk stores / reduce-adds of the partial rows
+#endif
 #ifndef GK_BWD_IL
 #define GK_BWD_IL 1  // interleave the replays of a slot pair in the real backward (C3 bwd 15.78 -> 15.60 ms)
 #endif
@@ -637,7 +640,8 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                 const int gs0 = gg * RG;
                 const int rho0 = gs0 % STEPS;
                 float *dst = a.partial + (((int64_t)blockIdx.x * (STEPS / RG) + rho0 / RG) * NW + warp) * (RG * OUTCH * 4);
-                if (gs0 < STEPS) bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
+                if (GK_NO_PARTIAL) {
+                } else if (gs0 < STEPS) bulk_s2g_store(dst, ob, (uint32_t)(RG * OUTCH * 16));
                 else bulk_s2g_reduce_add(dst, ob, (uint32_t)(RG * OUTCH * 16));
                 bulk_commit();
                 // successive slabs add into the same partial rows: keep them ordered

@@ -3,7 +3,7 @@
 // (or I to build U), and the replay backward with a deterministic dtheta reduction.
 //
 // Kernels (DESIGN.md §4 lists the roofline and algorithmic bytes of each):
-//   k_flip / k_sigma_* / k_coef  per-call coefficient precompute (fp64 trig, pi-reduction, sign
+//   k_sigma_bits / k_coef        per-call coefficient precompute (fp64 trig, pi-reduction, sign
 //                              bookkeeping) into the ring kernels' lane-chunked table layout;
 //   k_ring<W,L,MODE>           the hot path: one CTA owns a column slab, every block b_r runs
 //                              on-chip from registers, coefficients stream in by TMA bulk copies;
@@ -263,7 +263,7 @@ struct AutoWs {
 };
 
 struct WsLayout {
-    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, flip, sig, sfin, lay, fgm, sfg, partial, scratch, total;
+    size_t coef, coef_ph, coef_pf, coef_pt, coef_ab, amap, sig, sfin, lay, fgm, sfg, partial, scratch, total;
 };
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
@@ -282,8 +282,7 @@ WsLayout ws_layout(const Cfg &c, int op, int64_t m) {
     L.coef_pt = off; if (uni) off = al256(off + rows * c.S * 32);  // adjoint pairs (p, -q, q, p)
     L.coef_ab = off; if (uni) off = al256(off + rows * c.S * 8);
     L.amap = off; off = al256(off + rows * c.S * 4);
-    L.flip = off; off = al256(off + (size_t)c.R * c.S);
-    L.sig = off; off = al256(off + (size_t)c.R * c.ne);
+    L.sig = off; off = al256(off + (size_t)c.ne * ((c.R + 31) / 32) * 4);  // sigma bits [label][block / 32]
     L.sfin = off; off = al256(off + (size_t)c.ne);
     L.lay = off; off = al256(off + (size_t)(c.ne + 2) * 4);
     L.fgm = off; off = al256(off + rows * 4);            // fast Givens: factoring bits per table row
@@ -341,7 +340,7 @@ __device__ __forceinline__ int lay_refl(const int32_t *__restrict__ lay, int ne,
 // theta -> the angle phi in [-pi/2, pi/2] with R(theta) = (-1)^flip R(phi). theta is
 // any real (theta in R^N): it is first reduced to [-pi, pi] by the exact fp64
 // remainder modulo 2 pi (R is 2 pi-periodic), then flipped by pi when |.| > pi/2, so the shear
-// coefficient tan(phi/2) stays in [-1, 1] for every theta. k_flip, k_coef and k_coef_u all use it,
+// coefficient tan(phi/2) stays in [-1, 1] for every theta. k_sigma_bits, k_coef and k_coef_u all use it,
 // so the flip bits and the table agree.
 __device__ __forceinline__ double reduce_angle(double th, int *flip) {
     double r = remainder(th, 6.283185307179586);
@@ -351,60 +350,61 @@ __device__ __forceinline__ double reduce_angle(double th, int *flip) {
     return r;
 }
 
-// (1) flip bit per (block, slot): |theta| > pi/2 => R(theta) = -R(theta -/+ pi).
-__global__ void k_flip(int n, int ne, const float *__restrict__ theta, const uint8_t *__restrict__ mask,
-                       const int32_t *__restrict__ lay, uint8_t *__restrict__ flip) {
-    int S = ne / 2, R = ne - 1;
-    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)R * S) return;
-    int r = (int)(idx / S), k = (int)(idx % S);
-    int64_t f = flat_of_bl(r, k, n, ne, lay_bye(lay, ne));
-    uint8_t fl = 0;
-    if (f >= 0 && (!mask || mask[f])) {
-        int fb;
-        reduce_angle((double)theta[f], &fb);
-        fl = (uint8_t)fb;
+// (1)+(2) sign bookkeeping, one kernel. The flip bit of a rotation: |theta| > pi/2 => R(theta) =
+// -R(theta -/+ pi); sigma of label i before block r (in forward order the blocks r' > r
+// come first) is the parity of the flips of the rotations on i in those blocks. One
+// CTA per label i: lane j of a warp computes the flip of block 32c + j (one angle load and one fp64
+// reduction per thread) and a ballot makes it the bit word c; then thread c turns word c into
+// sigw[i][c] (bit j = sigma of label i before block 32c + j): the in-word exclusive suffix parity by a
+// shift-XOR scan, XOR the parity of all higher words (ballot + shared memory across warps). A
+// reflection D (applied before every block) flips the parity of its label in every block and in sfin;
+// the kernels then load and store without knowing about it. blockDim = 32 min(RW, 32),
+// RW = ceil((n_eff - 1) / 32) words per label (<= 1024).
+__global__ void __launch_bounds__(1024) k_sigma_bits(int n, int ne, const float *__restrict__ theta,
+                                                     const uint8_t *__restrict__ mask, const int32_t *__restrict__ lay,
+                                                     int refl, uint32_t *__restrict__ sigw, uint8_t *__restrict__ sfin) {
+    __shared__ uint32_t words[1024];
+    __shared__ uint32_t wpar[32];
+    const int R = ne - 1, RW = (R + 31) / 32, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarp = blockDim.x >> 5;
+    const int i = blockIdx.x;
+    const int bl = lay_bye(lay, ne);
+    for (int c = warp; c < RW; c += nwarp) {
+        const int r = 32 * c + lane;
+        int fl = 0;
+        if (r < R) {
+            const int p = pos_of(i, r, ne);
+            const int k = p < ne - 1 - p ? p : ne - 1 - p;
+            const int64_t f = flat_of_bl(r, k, n, ne, bl);
+            if (f >= 0 && (!mask || mask[f])) reduce_angle((double)theta[f], &fl);
+        }
+        const uint32_t fb = __ballot_sync(0xffffffffu, fl != 0);
+        if (lane == 0) words[c] = fb;
     }
-    flip[idx] = fl;
-}
-
-// (2) per row: parity of flips among the blocks applied before block r in forward order
-// (forward applies b_R first), i.e. blocks r' > r. sig[r][row], sfin[row].
-// The R blocks are cut into 32 contiguous segments (segment 0 = the highest blocks); thread
-// (row i, segment c) walks its segment: k_sigma_seg stores the segment's XOR, k_sigma_fill
-// starts from the XOR of the segments before it and writes sig. Consecutive threads take
-// consecutive rows, whose slots in a block are adjacent, so the flip reads are coalesced.
-// A reflection D (applied before every block) flips the parity of its label in every block and
-// in sfin; the kernels then load and store without knowing about it.
-__device__ __forceinline__ uint32_t flip_of(const uint8_t *__restrict__ flip, int i, int r, int ne) {
-    const int p = pos_of(i, r, ne);
-    const int k = p < ne - 1 - p ? p : ne - 1 - p;
-    return (uint32_t)flip[(int64_t)r * (ne / 2) + k];
-}
-
-// One kernel: a CTA of 32 rows x 32 segments; thread (row i, segment c) XORs its segment's flips into
-// shared memory, then starts from the XOR of the segments before it and writes sig (and sfin).
-__global__ void __launch_bounds__(1024) k_sigma(int ne, const uint8_t *__restrict__ flip,
-                                                const int32_t *__restrict__ lay, int refl,
-                                                uint8_t *__restrict__ sig, uint8_t *__restrict__ sfin) {
-    __shared__ uint8_t segx[32][33];
-    const int R = ne - 1, tx = threadIdx.x, c = threadIdx.y, i = blockIdx.x * 32 + tx;
-    const int seg = (R + 31) / 32, hi = R - 1 - c * seg, lo = max(hi - seg + 1, 0);
-    uint32_t x = 0;
-    if (i < ne)
-        for (int r = hi; r >= lo; r--) x ^= flip_of(flip, i, r, ne);
-    segx[c][tx] = (uint8_t)x;
     __syncthreads();
-    if (i >= ne) return;
-    uint32_t par = 0;
-    for (int cc = 0; cc < c; cc++) par ^= segx[cc][tx];
-    const uint32_t rf = (lay_refl(lay, ne, refl) == i) ? 1u : 0u;
-    if (c == 31) sfin[i] = (uint8_t)(par ^ segx[31][tx] ^ rf);
-    par ^= rf;
-    for (int r = hi; r >= lo; r--) {
-        sig[(int64_t)r * ne + i] = (uint8_t)par;
-        par ^= flip_of(flip, i, r, ne);
+    const uint32_t fb = tid < RW ? words[tid] : 0u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, (__popc(fb) & 1u) != 0);
+    if (lane == 0) wpar[warp] = __popc(bal) & 1u;
+    __syncthreads();
+    uint32_t carry = __popc(bal & (lane == 31 ? 0u : (0xffffffffu << (lane + 1)))) & 1u;  // higher words, my warp
+    uint32_t total = 0;
+    for (int v = 0; v < nwarp; v++) {
+        total ^= wpar[v];
+        if (v > warp) carry ^= wpar[v];
     }
+    if (tid >= RW) return;
+    uint32_t x = fb;  // inclusive suffix parity within the word: bit j = XOR of bits j..31
+    x ^= x >> 1;
+    x ^= x >> 2;
+    x ^= x >> 4;
+    x ^= x >> 8;
+    x ^= x >> 16;
+    const uint32_t rf = (lay_refl(lay, ne, refl) == i) ? 1u : 0u;
+    sigw[(int64_t)i * RW + tid] = (x >> 1) ^ ((carry ^ rf) ? 0xffffffffu : 0u);
+    if (tid == 0) sfin[i] = (uint8_t)(total ^ rf);
+}
+__device__ __forceinline__ int sig_bit(const uint32_t *__restrict__ sigw, int RW, int lab, int r) {
+    return (int)((sigw[(int64_t)lab * RW + (r >> 5)] >> (r & 31)) & 1u);
 }
 
 __device__ __forceinline__ int coef_pos(int k, int W, int L) {
@@ -418,9 +418,8 @@ __device__ __forceinline__ int coef_pos(int k, int W, int L) {
 // sgn * (tan(phi/2), sin(phi)) with phi the pi-reduced angle and sgn = sigma_top * sigma_bottom *
 // orientation (top row < bottom row); amap[rho][k] = flat | neg<<30 | masked<<29, or -1.
 __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *__restrict__ theta,
-                       const uint8_t *__restrict__ mask, const uint8_t *__restrict__ flip,
-                       const uint8_t *__restrict__ sig, const int32_t *__restrict__ lay, uint8_t *__restrict__ coef,
-                       int32_t *__restrict__ amap) {
+                       const uint8_t *__restrict__ mask, const uint32_t *__restrict__ sigw,
+                       const int32_t *__restrict__ lay, uint8_t *__restrict__ coef, int32_t *__restrict__ amap) {
     int S = ne / 2, R = ne - 1;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (int64_t)(R + 2) * S) return;
@@ -438,7 +437,8 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
     bool active = f >= 0 && (!mask || mask[f]);
     double th = active ? (double)theta[f] : 0.0;
     const double phi = reduce_angle(th, nullptr);
-    int neg = (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) ^ (lay_row(lay, a) > lay_row(lay, b) ? 1 : 0);
+    const int RW = (R + 31) / 32;
+    int neg = (sig_bit(sigw, RW, a, r) ^ sig_bit(sigw, RW, b, r)) ^ (lay_row(lay, a) > lay_row(lay, b) ? 1 : 0);
     double tq = tan(0.5 * phi), sq = sin(phi);
     if (neg) { tq = -tq; sq = -sq; }
     row[pos] = make_float2((float)tq, (float)sq);
@@ -453,7 +453,7 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
 // (1, 0) on the other. ab[rho][slot] = (alpha, beta): the dphi weights, w = alpha z_t + beta z_b
 // = cos(th_r) z_i + sigma_i sigma_j sin(th_r) z_j, th_r the pi-reduced angle.
 __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ theta, const float *__restrict__ phi,
-                         const uint8_t *__restrict__ mask, const uint8_t *__restrict__ sig,
+                         const uint8_t *__restrict__ mask, const uint32_t *__restrict__ sigw,
                          const int32_t *__restrict__ lay, float4 *__restrict__ ph, float4 *__restrict__ pf,
                          float4 *__restrict__ pt, float2 *__restrict__ ab) {
     int S = ne / 2, R = ne - 1;
@@ -491,7 +491,7 @@ __global__ void k_coef_u(int n, int ne, int W, int L, const float *__restrict__ 
         pt[pp1] = top_is_i ? one : c;
     }
     double cr = cos(thr), sr = sin(thr);
-    if (sig[(int64_t)r * ne + a] ^ sig[(int64_t)r * ne + b]) sr = -sr;
+    if (sig_bit(sigw, (R + 31) / 32, a, r) ^ sig_bit(sigw, (R + 31) / 32, b, r)) sr = -sr;
     abr[pos_ab] = top_is_i ? make_float2((float)cr, (float)sr) : make_float2((float)sr, (float)cr);
 }
 
@@ -919,7 +919,6 @@ constexpr Lay kNoLay{nullptr, -1};
 
 int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask, uint8_t *ws, const WsLayout &L,
                    cudaStream_t st, const float *phi = nullptr, Lay lo = kNoLay) {
-    int64_t RS = (int64_t)c.R * c.S;
     untag_tables(ws);  // partially rebuilt tables must not pass for the old ones if a launch fails
     // the layout block only under a start permutation (the kernels take lay == NULL as the identity)
     int32_t *lay = nullptr;
@@ -928,19 +927,21 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
         k_layout<<<1, 1024, 0, st>>>(n, c.ne, lo.perm, lo.refl, lay);
         CUDA_TRY(cudaGetLastError());
     }
-    k_flip<<<(unsigned)((RS + 255) / 256), 256, 0, st>>>(n, c.ne, theta, mask, lay, ws + L.flip);
-    CUDA_TRY(cudaGetLastError());
-    k_sigma<<<(unsigned)((c.ne + 31) / 32), dim3(32, 32), 0, st>>>(c.ne, ws + L.flip, lay, lo.refl, ws + L.sig,
-                                                                     ws + L.sfin);
-    CUDA_TRY(cudaGetLastError());
+    {
+        const int RW = (c.R + 31) / 32;
+        k_sigma_bits<<<(unsigned)c.ne, (unsigned)(32 * std::min(RW, 32)), 0, st>>>(
+            n, c.ne, theta, mask, lay, lo.refl, reinterpret_cast<uint32_t *>(ws + L.sig), ws + L.sfin);
+        CUDA_TRY(cudaGetLastError());
+    }
     int64_t tot = (int64_t)(c.R + 2) * c.S;
     int W = c.fast ? c.W : c.S, Lq = c.fast ? c.La : 1;
-    k_coef<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, c.rowbytes, theta, mask, ws + L.flip,
-                                                          ws + L.sig, lay, ws + L.coef,
+    k_coef<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, c.rowbytes, theta, mask,
+                                                          reinterpret_cast<const uint32_t *>(ws + L.sig), lay, ws + L.coef,
                                                           reinterpret_cast<int32_t *>(ws + L.amap));
     CUDA_TRY(cudaGetLastError());
     if (phi) {
-        k_coef_u<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, theta, phi, mask, ws + L.sig, lay,
+        k_coef_u<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, theta, phi, mask,
+                                                                reinterpret_cast<const uint32_t *>(ws + L.sig), lay,
                                                                 reinterpret_cast<float4 *>(ws + L.coef_ph),
                                                                 reinterpret_cast<float4 *>(ws + L.coef_pf),
                                                                 reinterpret_cast<float4 *>(ws + L.coef_pt),
