@@ -89,6 +89,9 @@ constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #ifndef GK_UNI_ONE_SITE
 #define GK_UNI_ONE_SITE 1  // unitary backward: one reduction call site per group (u_backward 63.3 -> 62.5 ms)
 #endif
+#ifndef GK_BFIRST
+#define GK_BFIRST 1  // two-warp-column backward: ring-boundary slot quads first in every step (see k_ring)
+#endif
 #ifndef GK_NO_PARTIAL
 #define GK_NO_PARTIAL 0  // timing ablation only (wrong dtheta): skip the bulk stores / reduce-adds of the partial rows
 #endif
@@ -476,6 +479,10 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                           UBH % G::SPS == 0 && (!GRAD || UBH % G::RG == 0) && UBH % 2 == 0;
     constexpr int UB = HALF ? UBH : W;  // steps per unrolled body
     constexpr bool FG = (MODE & M_FG) != 0;
+    // (measured, one box: two-warp-column backward C5 shard 37.2 -> 35.8 ms, n = 2048 U-build gradient
+    // 2.78 -> 2.76 ms; slower for one-warp columns (C3 backward 15.58 -> 15.78 ms), the forwards and
+    // four-warp columns, which keep the natural order)
+    constexpr bool BFIRST = GK_BFIRST != 0 && H == 2 && GRAD;
     static_assert(!FG || (L == 1 && !UNI && !GRAD && !UP), "fast Givens: forward / U-build on one-lane columns");
 
     extern __shared__ __align__(128) uint8_t smem[];
@@ -822,7 +829,14 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
 #pragma unroll
                 for (int jj = 0; jj < W / 2; jj++) {
                     // DEFER: middle pairs 1 .. W/2-2 first, then the two boundary pairs
-                    const int pp = !DEFER ? jj : (jj < W / 2 - 2 ? jj + 1 : (jj == W / 2 - 2 ? 0 : W / 2 - 1));
+                    // BFIRST: the quads (4 slots) holding the two ring-boundary slots 0 and W-1 go first, so the
+                    // step's shift shuffles (of the rotated T[W-1] and B[0]) can issue half way through the
+                    // step and the next step's boundary slots find them done; quads stay contiguous for the
+                    // per-quad dtheta ring stores
+                    constexpr int NQ = W / 4;
+                    const int qd = jj / 2, qp = (!BFIRST || NQ <= 2) ? qd : (qd == 0 ? 0 : (qd == 1 ? NQ - 1 : qd - 1));
+                    const int pp = !DEFER ? 2 * qp + (jj & 1)
+                                          : (jj < W / 2 - 2 ? jj + 1 : (jj == W / 2 - 2 ? 0 : W / 2 - 1));
                     if constexpr (DEFER) {
                         if (jj == W / 2 - 2 && xpend) {
                             constexpr int ppar = (uu + 1) & 1;  // parity of the previous step's buffers

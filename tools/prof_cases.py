@@ -2,8 +2,8 @@
 hot-path case with the bench's synthetic inputs, so a launch list / --set full capture can be taken
 of exactly the kernels that case launches.
 
-cases: c3 (n=1024, m=65536 apply + backward), c2 (n=256, m=4096), ub1024 (build_U + gradient,
-n=1024), c4 (build_U + gradient, n=4096), c5 (n=2047, m=32768, mask m_keep=1024), unitary
+cases: c3 (n=1024, m=65536 apply + backward), c2 (n=256, m=4096), ubN (build_U + gradient,
+n=N, e.g. ub1024), c4 (build_U + gradient, n=4096), c5 (n=2047, m=32768, mask m_keep=1024), unitary
 (n=1024, 32768 complex columns), gemm (the f2 GEMM path at C3)."""
 import argparse
 import os
@@ -54,8 +54,8 @@ elif a.case == "c2":
     real_case(256, 4096)
 elif a.case == "c5":
     real_case(2047, 32768, mask_keep=1024)
-elif a.case == "ub1024":
-    ubuild_case(1024)
+elif a.case.startswith("ub"):
+    ubuild_case(int(a.case[2:]))
 elif a.case == "c4":
     ubuild_case(4096)
 elif a.case == "unitary":
