@@ -89,6 +89,9 @@ constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #ifndef GK_UNI_ONE_SITE
 #define GK_UNI_ONE_SITE 1  // unitary backward: one reduction call site per group (u_backward 63.3 -> 62.5 ms)
 #endif
+#ifndef GK_DEFER_BWD
+#define GK_DEFER_BWD 1  // the backward's warp-boundary exchange "arrive early, wait late" (bit 0: four-warp, bit 1: two-warp columns)
+#endif
 #ifndef GK_BFIRST
 #define GK_BFIRST 1  // two-warp-column backward: ring-boundary slot quads first in every step (see k_ring)
 #endif
@@ -472,7 +475,9 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     // before it is read. Measured (one B200, same call): four-warp columns (n = 4096 U-build) 7.21 ->
     // 6.99 ms; two-warp columns got slower (C5 shard forward 10.94 -> 11.63 ms), so they keep the
     // named barrier.
-    constexpr bool DEFER = (H >= 4) && !GRAD;
+    // (the backward too, under GK_DEFER_BWD: bit 0 four-warp columns, bit 1 two-warp columns; its
+    // boundary values include D, and its slot order keeps the quads whole for the dtheta ring stores)
+    constexpr bool DEFER = !GRAD ? (H >= 4) : (!UNI && (((GK_DEFER_BWD & 1) && H >= 4) || ((GK_DEFER_BWD & 2) && H == 2)));
     constexpr int UBH = W / 2;
     constexpr bool HALF = ((UNI && GRAD && (GK_HALF_BODY & 1)) || (UNI && !GRAD && (GK_HALF_BODY & 2)) ||
                            (!UNI && GRAD && (GK_HALF_BODY & 4)) || (!UNI && !GRAD && (GK_HALF_BODY & 8))) &&
@@ -699,6 +704,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             for (int p = 0; p < KP; p++) {
                 if (UP) ZT[p][0] = xprev[XV + p];
                 else ZB[p][0] = xprev[XV + p];
+                if constexpr (GRAD) DT[p][0] = xprev[XV + KP + p];
             }
         }
         if (lane == 31 && h < H - 1) {
@@ -706,6 +712,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
             for (int p = 0; p < KP; p++) {
                 if (UP) ZB[p][W - 1] = xnext[p];
                 else ZT[p][W - 1] = xnext[p];
+                if constexpr (GRAD) DB[p][W - 1] = xnext[KP + p];
             }
         }
     };
@@ -835,10 +842,13 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     // per-quad dtheta ring stores
                     constexpr int NQ = W / 4;
                     const int qd = jj / 2, qp = (!BFIRST || NQ <= 2) ? qd : (qd == 0 ? 0 : (qd == 1 ? NQ - 1 : qd - 1));
+                    // DEFER backward: middle quads first, then quad 0 and quad NQ-1 (whole quads)
+                    const int qg = qd < NQ - 2 ? qd + 1 : (qd == NQ - 2 ? 0 : NQ - 1);
                     const int pp = !DEFER ? 2 * qp + (jj & 1)
-                                          : (jj < W / 2 - 2 ? jj + 1 : (jj == W / 2 - 2 ? 0 : W / 2 - 1));
+                                 : GRAD ? 2 * qg + (jj & 1)
+                                        : (jj < W / 2 - 2 ? jj + 1 : (jj == W / 2 - 2 ? 0 : W / 2 - 1));
                     if constexpr (DEFER) {
-                        if (jj == W / 2 - 2 && xpend) {
+                        if (jj == (GRAD ? W / 2 - 4 : W / 2 - 2) && xpend) {
                             constexpr int ppar = (uu + 1) & 1;  // parity of the previous step's buffers
                             mbar_wait(&xb[cw], (uint32_t)((xn - 1) & 1));
                             xpatch(ppar);
