@@ -84,7 +84,7 @@ enum Mode { M_FWD = 0, M_BUILDU = 1, M_TRANS = 2, M_BWD = 3, M_UNI = 4, M_IDLE =
             M_FG = 64 };
 constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #ifndef GK_HALF_BODY
-#define GK_HALF_BODY 0  // bit mask (1 unitary bwd, 2 unitary fwd, 4 real bwd, 8 real fwd): W/2-step bodies
+#define GK_HALF_BODY -1  // -1: per-kernel choice (k_ring); else bit mask (1 unitary bwd, 2 unitary fwd, 4 real bwd, 8 real fwd): W/2-step bodies
 #endif
 #ifndef GK_UNI_ONE_SITE
 #define GK_UNI_ONE_SITE 1  // unitary backward: one reduction call site per group (u_backward 63.3 -> 62.5 ms)
@@ -479,9 +479,18 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     // boundary values include D, and its slot order keeps the quads whole for the dtheta ring stores)
     constexpr bool DEFER = !GRAD ? (H >= 4) : (!UNI && (((GK_DEFER_BWD & 1) && H >= 4) || ((GK_DEFER_BWD & 2) && H == 2)));
     constexpr int UBH = W / 2;
-    constexpr bool HALF = ((UNI && GRAD && (GK_HALF_BODY & 1)) || (UNI && !GRAD && (GK_HALF_BODY & 2)) ||
-                           (!UNI && GRAD && (GK_HALF_BODY & 4)) || (!UNI && !GRAD && (GK_HALF_BODY & 8))) &&
-                          UBH % G::SPS == 0 && (!GRAD || UBH % G::RG == 0) && UBH % 2 == 0;
+    // W/2-step unrolled bodies: half the instruction footprint, for a register move of the ring at every
+    // loop edge (the renaming is half way round). Chosen per kernel from one-box A/B runs of the whole
+    // library (GK_HALF_BODY=15 against 0): the unitary backward 62.4 -> 38.7 ms and apply 12.9 -> 11.9 ms
+    // (no_instruction was 2.8 stalls per issue), the n = 1024 U-build gradient (W = 16 narrow) 488 -> 403 us,
+    // C4 gradient 21.6 -> 20.9 ms, C5 shard backward 35.9 -> 35.3 ms; slower for the one-warp-column wide
+    // backward (C3 15.62 -> 15.82 ms), the real forwards (C5 shard 10.93 -> 11.3 ms) and the W = 8
+    // narrow backward (n = 256 gradient 67.0 -> 69.4 us), which keep W-step bodies
+    constexpr bool HALF_PICK = GK_HALF_BODY >= 0
+                                   ? ((UNI && GRAD && (GK_HALF_BODY & 1)) || (UNI && !GRAD && (GK_HALF_BODY & 2)) ||
+                                      (!UNI && GRAD && (GK_HALF_BODY & 4)) || (!UNI && !GRAD && (GK_HALF_BODY & 8)))
+                                   : (UNI || (GRAD && (H >= 2 || ((MODE & M_NARROW) && W == 16))));
+    constexpr bool HALF = HALF_PICK && UBH % G::SPS == 0 && (!GRAD || UBH % G::RG == 0) && UBH % 2 == 0;
     constexpr int UB = HALF ? UBH : W;  // steps per unrolled body
     constexpr bool FG = (MODE & M_FG) != 0;
     // (measured, one box: two-warp-column backward C5 shard 37.2 -> 35.8 ms, n = 2048 U-build gradient
