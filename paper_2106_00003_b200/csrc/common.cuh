@@ -86,6 +86,11 @@ constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #ifndef GK_HALF_BODY
 #define GK_HALF_BODY -1  // -1: per-kernel choice (k_ring); else bit mask (1 unitary bwd, 2 unitary fwd, 4 real bwd, 8 real fwd): W/2-step bodies
 #endif
+#ifndef GK_QUARTER_BODY
+#define GK_QUARTER_BODY 2  // bit mask as GK_HALF_BODY: W/4-step bodies (the unitary apply: 11.88 -> 11.71 ms; the
+                           // others measured neutral or slower: C5 shard backward 35.26 -> 36.2 ms, C4 gradient
+                           // 20.96 -> 21.26 ms, unitary backward 38.63 -> 38.75 ms)
+#endif
 #ifndef GK_UNI_ONE_SITE
 #define GK_UNI_ONE_SITE 1  // unitary backward: one reduction call site per group (u_backward 63.3 -> 62.5 ms)
 #endif
@@ -491,7 +496,13 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                                       (!UNI && GRAD && (GK_HALF_BODY & 4)) || (!UNI && !GRAD && (GK_HALF_BODY & 8)))
                                    : (UNI || (GRAD && (H >= 2 || ((MODE & M_NARROW) && W == 16))));
     constexpr bool HALF = HALF_PICK && UBH % G::SPS == 0 && (!GRAD || UBH % G::RG == 0) && UBH % 2 == 0;
-    constexpr int UB = HALF ? UBH : W;  // steps per unrolled body
+    // W/4-step bodies (GK_QUARTER_BODY, same bit mask as GK_HALF_BODY; where the stage and ring group
+    // sizes divide W/4)
+    constexpr int UBQ = W / 4;
+    constexpr bool QUARTER = ((UNI && GRAD && (GK_QUARTER_BODY & 1)) || (UNI && !GRAD && (GK_QUARTER_BODY & 2)) ||
+                              (!UNI && GRAD && (GK_QUARTER_BODY & 4)) || (!UNI && !GRAD && (GK_QUARTER_BODY & 8))) &&
+                             UBQ % G::SPS == 0 && (!GRAD || UBQ % G::RG == 0) && UBQ % 2 == 0;
+    constexpr int UB = QUARTER ? UBQ : (HALF ? UBH : W);  // steps per unrolled body
     constexpr bool FG = (MODE & M_FG) != 0;
     // (measured, one box: two-warp-column backward C5 shard 37.2 -> 35.8 ms, n = 2048 U-build gradient
     // 2.78 -> 2.76 ms; slower for one-warp columns (C3 backward 15.58 -> 15.78 ms), the forwards and
