@@ -100,6 +100,9 @@ constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #ifndef GK_BFIRST
 #define GK_BFIRST 1  // two-warp-column backward: ring-boundary slot quads first in every step (see k_ring)
 #endif
+#ifndef GK_PDL
+#define GK_PDL 1  // programmatic dependent launches of k_coef, the ring kernels and the stage-2 reduction
+#endif
 #ifndef GK_NO_PARTIAL
 #define GK_NO_PARTIAL 0  // timing ablation only (wrong dtheta): skip the bulk stores / reduce-adds of the partial rows
 #endif
@@ -146,6 +149,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
     while (!mbar_try(b, parity)) {
     }
 }
+
+// Programmatic dependent launch: a kernel launched with the programmatic-stream-serialization
+// attribute may start before its predecessor on the stream has finished; it must not touch memory the
+// predecessor writes (or reads) before pdl_wait(), which returns once the predecessor has completed and
+// its writes are visible. pdl_trigger() lets the successor launch as soon as every CTA of this grid has
+// issued it. Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 // compile-time unrolling: f(std::integral_constant<int, I>{}) for I = 0..N-1, as straight-line code
 template <typename F, int... I>
@@ -552,6 +563,10 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
         fence_proxy_async_smem();
     }
     __syncthreads();
+    // launched with programmatic stream serialization (launch_wlm): the barrier setup above overlaps the
+    // predecessor's tail; every global access (tables, signs, X, outputs) comes after this wait
+    pdl_trigger();
+    pdl_wait();
     if constexpr (GRAD) {
         // pre-arm: every ring group starts out "empty" (phase 0 completes here), so the first
         // use of each group waits on parity 0 without a special case

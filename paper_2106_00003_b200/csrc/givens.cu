@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(1024) k_sigma_bits(int n, int ne, const float 
     __shared__ uint32_t wpar[32];
     const int R = ne - 1, RW = (R + 31) / 32, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nwarp = blockDim.x >> 5;
+    pdl_trigger();  // k_coef may start its trigonometry (it waits for these bits)
     const int i = blockIdx.x;
     const int bl = lay_bye(lay, ne);
     for (int c = warp; c < RW; c += nwarp) {
@@ -421,25 +422,38 @@ __global__ void k_coef(int n, int ne, int W, int L, int rowbytes, const float *_
                        const uint8_t *__restrict__ mask, const uint32_t *__restrict__ sigw,
                        const int32_t *__restrict__ lay, uint8_t *__restrict__ coef, int32_t *__restrict__ amap) {
     int S = ne / 2, R = ne - 1;
-    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= (int64_t)(R + 2) * S) return;
-    int rho = (int)(idx / S), k = (int)(idx % S);
+    pdl_trigger();
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = idx < (int64_t)(R + 2) * S;
+    const int rho = (int)(idx / S), k = (int)(idx % S);
+    const bool pad = rho == 0 || rho == R + 1;
+    const int r = rho - 1;
+    int a = 0, b = 0;
+    int64_t f = -1;
+    bool active = false;
+    double tq = 0.0, sq = 0.0;
+    if (live && !pad) {
+        a = seq_at(r, k, ne);  // labels; rows lay[a], lay[b]
+        b = seq_at(r, ne - 1 - k, ne);
+        f = flat_of_bl(r, k, n, ne, lay_bye(lay, ne));
+        active = f >= 0 && (!mask || mask[f]);
+        const double phi = reduce_angle(active ? (double)theta[f] : 0.0, nullptr);
+        tq = tan(0.5 * phi);
+        sq = sin(phi);
+    }
+    // (launched dependent on k_sigma_bits: the trigonometry above overlaps it; the sign bits are its
+    // output. Every thread waits, so this grid cannot complete before its predecessor.)
+    pdl_wait();
+    if (!live) return;
     float2 *row = reinterpret_cast<float2 *>(coef + (int64_t)rho * rowbytes);
-    int pos = coef_pos(k, W, L);
-    if (rho == 0 || rho == R + 1) {
+    const int pos = coef_pos(k, W, L);
+    if (pad) {
         row[pos] = make_float2(0.f, 0.f);
         amap[(int64_t)rho * S + k] = -1;
         return;
     }
-    int r = rho - 1;
-    int a = seq_at(r, k, ne), b = seq_at(r, ne - 1 - k, ne);  // labels; rows lay[a], lay[b]
-    int64_t f = flat_of_bl(r, k, n, ne, lay_bye(lay, ne));
-    bool active = f >= 0 && (!mask || mask[f]);
-    double th = active ? (double)theta[f] : 0.0;
-    const double phi = reduce_angle(th, nullptr);
     const int RW = (R + 31) / 32;
     int neg = (sig_bit(sigw, RW, a, r) ^ sig_bit(sigw, RW, b, r)) ^ (lay_row(lay, a) > lay_row(lay, b) ? 1 : 0);
-    double tq = tan(0.5 * phi), sq = sin(phi);
     if (neg) { tq = -tq; sq = -sq; }
     row[pos] = make_float2((float)tq, (float)sq);
     int32_t code = -1;
@@ -917,6 +931,30 @@ struct Lay {
 };
 constexpr Lay kNoLay{nullptr, -1};
 
+// a launch with the programmatic-stream-serialization attribute (pdl_wait / pdl_trigger, common.cuh)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kfn)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = GK_PDL ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kfn, static_cast<KArgs>(args)...);
+}
+
+// the same without the attribute: the stage-2 reduction (launched early, its small CTAs would sit
+// beside the latency-bound ring CTAs on the same SMs while they wait; measured slower at n = 1024)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_plain(void (*kfn)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
+    kfn<<<grid, block, 0, st>>>(static_cast<KArgs>(args)...);
+    return cudaGetLastError();
+}
+
 int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask, uint8_t *ws, const WsLayout &L,
                    cudaStream_t st, const float *phi = nullptr, Lay lo = kNoLay) {
     untag_tables(ws);  // partially rebuilt tables must not pass for the old ones if a launch fails
@@ -935,10 +973,9 @@ int run_precompute(const Cfg &c, int n, const float *theta, const uint8_t *mask,
     }
     int64_t tot = (int64_t)(c.R + 2) * c.S;
     int W = c.fast ? c.W : c.S, Lq = c.fast ? c.La : 1;
-    k_coef<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, c.rowbytes, theta, mask,
-                                                          reinterpret_cast<const uint32_t *>(ws + L.sig), lay, ws + L.coef,
-                                                          reinterpret_cast<int32_t *>(ws + L.amap));
-    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(launch_pdl(k_coef, (unsigned)((tot + 255) / 256), 256, st, n, c.ne, W, Lq, c.rowbytes, theta, mask,
+                        reinterpret_cast<const uint32_t *>(ws + L.sig), lay, ws + L.coef,
+                        reinterpret_cast<int32_t *>(ws + L.amap)));
     if (phi) {
         k_coef_u<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(n, c.ne, W, Lq, theta, phi, mask,
                                                                 reinterpret_cast<const uint32_t *>(ws + L.sig), lay,
@@ -1187,11 +1224,10 @@ int givens_u_backward_ex(int32_t n, int64_t m, const float *theta, const float *
     if ((rc = run_apply_mode(M_BWD | M_UNI, n, 2 * m, Y, 2 * ldy, dY, 2 * lddy, dX, 2 * lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD | M_UNI, 2 * m);
     const int64_t tot = (int64_t)2 * c.S * c.S;
-    k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+    CUDA_TRY(launch_plain(k_dtheta_reduce, (unsigned)((tot + 255) / 256), 256, st,
         c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD | M_UNI, 2 * m)), (int)G, c.fast, 2,
         reinterpret_cast<const float *>(w + L.partial),
-        reinterpret_cast<const int32_t *>(w + L.amap), dtheta, dphi);
-    CUDA_TRY(cudaGetLastError());
+        reinterpret_cast<const int32_t *>(w + L.amap), dtheta, dphi));
     return 0;
 }
 
@@ -1260,11 +1296,10 @@ int givens_backward_ex(int32_t n, int64_t m, const float *theta, const uint8_t *
     if ((rc = run_apply_mode(M_BWD, n, m, Y, ldy, dY, lddy, dX, lddx, w, L, c, st, perm))) return rc;
     int64_t G = grid_for(c, M_BWD, m);
     const int64_t tot = (int64_t)2 * c.S * c.S;
-    k_dtheta_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(
+    CUDA_TRY(launch_plain(k_dtheta_reduce, (unsigned)((tot + 255) / 256), 256, st,
         c.S, c.fast ? c.W : c.S, c.fast ? c.L : 1, ring_warps(launch_mode(c, M_BWD, m)), (int)G, c.fast, 1,
         reinterpret_cast<const float *>(w + L.partial), reinterpret_cast<const int32_t *>(w + L.amap),
-        dtheta, nullptr);
-    CUDA_TRY(cudaGetLastError());
+        dtheta, nullptr));
     return 0;
 }
 

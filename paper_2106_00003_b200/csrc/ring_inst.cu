@@ -14,12 +14,30 @@ namespace gk {
 
 template <int W, int L, int MODE>
 static cudaError_t launch_wlm(const RingArgs &ra, int64_t grid, cudaStream_t st) {
-    constexpr size_t smem = RingGeom<W, L, MODE>::SMEM;
+    // at least 120 KB: one CTA per SM (the grids are sized for that, grid_for), also when the CTAs of a
+    // programmatic dependent launch become resident while the predecessor still runs (measured: without
+    // the floor the 64 KB narrow C2 forward CTAs doubled up on SMs, 41 -> 57 us)
+    constexpr size_t smem = RingGeom<W, L, MODE>::SMEM > 120 * 1024 ? RingGeom<W, L, MODE>::SMEM : 120 * 1024;
     static_assert(smem <= 227 * 1024, "shared memory budget");
     auto kfn = k_ring<W, L, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kfn<<<(unsigned)grid, RingGeom<W, L, MODE>::NW * 32, smem, st>>>(ra);
+    // programmatic dependent launch (see pdl_wait in common.cuh): the CTAs may start while the
+    // precompute / the previous ring kernel drains
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(RingGeom<W, L, MODE>::NW * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    // (narrow launches only: the latency regime gains -- n = 256 build 30.8 -> 26.7 us, C2 142 -> 136 us
+    // -- while the four-warp-column U-build measured 6.98 -> 7.17 ms with it)
+    cfg.numAttrs = (GK_PDL && (MODE & M_NARROW)) ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kfn, ra);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
