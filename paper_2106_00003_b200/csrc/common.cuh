@@ -103,6 +103,12 @@ constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #ifndef GK_PDL
 #define GK_PDL 1  // programmatic dependent launches of k_coef, the ring kernels and the stage-2 reduction
 #endif
+#ifndef GK_XPRED
+#define GK_XPRED 1  // multi-warp columns (named-barrier exchange): branch-free warp-boundary publish / read
+                    // (C5 shard forward 10.93 -> 9.63 ms, backward 35.26 -> 33.56 ms; n = 2048 U-build
+                    // 0.855 -> 0.750 ms, gradient 2.746 -> 2.632 ms: the per-step divergent regions around the
+                    // lane-0 / lane-31 stores and loads had cost 8.5% branch_resolving stall samples)
+#endif
 #ifndef GK_NO_PARTIAL
 #define GK_NO_PARTIAL 0  // timing ablation only (wrong dtheta): skip the bulk stores / reduce-adds of the partial rows
 #endif
@@ -157,6 +163,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
 // issued it. Both are no-ops for a kernel launched without the attribute.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// predicated shared-memory store (no divergent branch around it)
+__device__ __forceinline__ void st_shared_if(bool p, float *a, float v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.f32 [%1], %2;\n}" ::"r"((uint32_t)p),
+                 "r"(smem_u32(a)), "f"(v)
+                 : "memory");
+}
+__device__ __forceinline__ void st_shared_if(bool p, float2 *a, float2 v) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q st.shared.v2.f32 [%1], {%2, %3};\n}" ::"r"((uint32_t)p),
+                 "r"(smem_u32(a)), "f"(v.x), "f"(v.y)
+                 : "memory");
+}
 
 // compile-time unrolling: f(std::integral_constant<int, I>{}) for I = 0..N-1, as straight-line code
 template <typename F, int... I>
@@ -1058,7 +1076,21 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     // values crossing a warp boundary: publish, named barrier of the group, read
                     constexpr int par = uu & 1;  // double buffer (W is even)
                     V *xo = xbuf + ((size_t)(par * NW + warp) * 2) * XV;  // [0]: to warp h-1, [1]: to warp h+1
-                    if (UP) {
+                    if (GK_XPRED && !DEFER) {
+                        // branch-free publish: lanes 0 and 31 store through predicated STS (no divergent
+                        // region per step), the same slots as below
+                        const bool pub = lane == 0 || lane == 31;
+#pragma unroll
+                        for (int p = 0; p < KP; p++) {
+                            if (UP) {
+                                st_shared_if(pub, xo + (lane == 31 ? XV + p : p), lane == 31 ? ZT[p][W - 1] : ZB[p][0]);
+                                if constexpr (GRAD)
+                                    st_shared_if(pub, xo + (lane == 31 ? XV + KP + p : KP + p), lane == 31 ? DT[p][W - 1] : DB[p][0]);
+                            } else {
+                                st_shared_if(pub, xo + (lane == 0 ? p : XV + p), lane == 0 ? ZT[p][0] : ZB[p][W - 1]);
+                            }
+                        }
+                    } else if (UP) {
                         // lane t+1 needs my T[W-1] (from_prev), lane t-1 needs my B[0] (from_next)
                         if (lane == 31) {
 #pragma unroll
@@ -1098,6 +1130,35 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     const V *xnext = xbuf + ((size_t)(par * NW + warp + 1) * 2) * XV;  // warp h+1
                     const bool from_x_prev = !DEFER && (lane == 0 && h > 0);
                     const bool from_x_next = !DEFER && (lane == 31 && h < H - 1);
+                    if constexpr (GK_XPRED && !DEFER) {
+                        // branch-free read: every lane loads (clamped, always valid addresses; one broadcast
+                        // wavefront each) and the two boundary lanes select
+                        const V *xp = xbuf + ((size_t)(par * NW + (h > 0 ? warp - 1 : warp)) * 2) * XV;
+                        const V *xq = xbuf + ((size_t)(par * NW + (h < H - 1 ? warp + 1 : warp)) * 2) * XV;
+#pragma unroll
+                        for (int p = 0; p < KP; p++) {
+                            if (UP) {
+                                const V lp = xp[XV + p], ln = xq[p];
+                                V fp = shfl_up_v(ZT[p][W - 1], 32), fn = shfl_dn_v(ZB[p][0], 32);
+                                fp = sel_v(from_x_prev, lp, fp);
+                                fn = sel_v(from_x_next, ln, fn);
+                                shift_up_with<W>(ZT[p], ZB[p], first, last, fp, fn);
+                                if constexpr (GRAD) {
+                                    const V lq = xp[XV + KP + p], lr = xq[KP + p];
+                                    V dp = shfl_up_v(DT[p][W - 1], 32), dn = shfl_dn_v(DB[p][0], 32);
+                                    dp = sel_v(from_x_prev, lq, dp);
+                                    dn = sel_v(from_x_next, lr, dn);
+                                    shift_up_with<W>(DT[p], DB[p], first, last, dp, dn);
+                                }
+                            } else {
+                                const V ln = xq[p], lp = xp[XV + p];
+                                V fn = shfl_dn_v(ZT[p][0], 32), fp = shfl_up_v(ZB[p][W - 1], 32);
+                                fn = sel_v(from_x_next, ln, fn);
+                                fp = sel_v(from_x_prev, lp, fp);
+                                shift_down_with<W>(ZT[p], ZB[p], first, last, fn, fp);
+                            }
+                        }
+                    } else {
 #pragma unroll
                     for (int p = 0; p < KP; p++) {
                         if (UP) {
@@ -1118,6 +1179,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                             shift_down_with<W>(ZT[p], ZB[p], first, last, fn, fp);
                         }
                     }
+                    }  // !GK_XPRED
                 }
                 if constexpr (su == SPS - 1) {
                     // release the stage buffer; the LAST warp to release it refills it with the
