@@ -104,7 +104,9 @@ constexpr int kNWN = 4;  // warps per CTA of the narrow variant
 #define GK_PDL 1  // programmatic dependent launches of k_coef, the ring kernels and the stage-2 reduction
 #endif
 #ifndef GK_XPRED
-#define GK_XPRED 1  // multi-warp columns (named-barrier exchange): branch-free warp-boundary publish / read
+#define GK_XPRED 3  // multi-warp columns: branch-free warp-boundary publish / read (bit 0: the named-barrier
+                    // exchange of two-warp columns; bit 1: also the deferred exchange of four-warp columns,
+                    // C4 U-build 7.06 -> 6.52 ms, gradient 20.81 -> 20.15 ms)
                     // (C5 shard forward 10.93 -> 9.63 ms, backward 35.26 -> 33.56 ms; n = 2048 U-build
                     // 0.855 -> 0.750 ms, gradient 2.746 -> 2.632 ms: the per-step divergent regions around the
                     // lane-0 / lane-31 stores and loads had cost 8.5% branch_resolving stall samples)
@@ -750,6 +752,29 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
     // buffers have parity ppar): forward (shift_down) lane 31's T[W-1] and lane 0's B[0]; backward
     // direction (shift_up, the transpose apply) lane 0's T[0] and lane 31's B[W-1]
     auto xpatch = [&](int ppar) {
+        if constexpr (GK_XPRED & 2) {
+            // branch-free: clamped broadcast loads, the two boundary lanes select
+            const V *xp = xbuf + ((size_t)(ppar * NW + (h > 0 ? warp - 1 : warp)) * 2) * XV;
+            const V *xq = xbuf + ((size_t)(ppar * NW + (h < H - 1 ? warp + 1 : warp)) * 2) * XV;
+            const bool fp = lane == 0 && h > 0, fq = lane == 31 && h < H - 1;
+#pragma unroll
+            for (int p = 0; p < KP; p++) {
+                const V a0 = xp[XV + p], b0 = xq[p];
+                if (UP) {
+                    ZT[p][0] = sel_v(fp, a0, ZT[p][0]);
+                    ZB[p][W - 1] = sel_v(fq, b0, ZB[p][W - 1]);
+                } else {
+                    ZB[p][0] = sel_v(fp, a0, ZB[p][0]);
+                    ZT[p][W - 1] = sel_v(fq, b0, ZT[p][W - 1]);
+                }
+                if constexpr (GRAD) {
+                    const V a1 = xp[XV + KP + p], b1 = xq[KP + p];
+                    DT[p][0] = sel_v(fp, a1, DT[p][0]);
+                    DB[p][W - 1] = sel_v(fq, b1, DB[p][W - 1]);
+                }
+            }
+            return;
+        }
         const V *xprev = xbuf + ((size_t)(ppar * NW + warp - 1) * 2) * XV;
         const V *xnext = xbuf + ((size_t)(ppar * NW + warp + 1) * 2) * XV;
         if (lane == 0 && h > 0) {
@@ -1076,7 +1101,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     // values crossing a warp boundary: publish, named barrier of the group, read
                     constexpr int par = uu & 1;  // double buffer (W is even)
                     V *xo = xbuf + ((size_t)(par * NW + warp) * 2) * XV;  // [0]: to warp h-1, [1]: to warp h+1
-                    if (GK_XPRED && !DEFER) {
+                    if ((GK_XPRED & 1) && (!DEFER || (GK_XPRED & 2))) {
                         // branch-free publish: lanes 0 and 31 store through predicated STS (no divergent
                         // region per step), the same slots as below
                         const bool pub = lane == 0 || lane == 31;
@@ -1130,7 +1155,7 @@ __global__ void __launch_bounds__(RingGeom<W, L, MODE>::NW * 32, 1) k_ring(const
                     const V *xnext = xbuf + ((size_t)(par * NW + warp + 1) * 2) * XV;  // warp h+1
                     const bool from_x_prev = !DEFER && (lane == 0 && h > 0);
                     const bool from_x_next = !DEFER && (lane == 31 && h < H - 1);
-                    if constexpr (GK_XPRED && !DEFER) {
+                    if constexpr ((GK_XPRED & 1) && !DEFER) {
                         // branch-free read: every lane loads (clamped, always valid addresses; one broadcast
                         // wavefront each) and the two boundary lanes select
                         const V *xp = xbuf + ((size_t)(par * NW + (h > 0 ? warp - 1 : warp)) * 2) * XV;
